@@ -1,0 +1,180 @@
+"""Pins for oracle/tensor.py and oracle/decomp.py (eqs. (10), (12),
+Algorithms 1-3).  Pins: worked unfolding example, brute-force loops, known-rank
+synthetic tensors, the HOSVD/TT/H-Tucker error bounds (theorems), degenerate
+inputs, and Table II's direction-mode rank."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import decomp, fmm, restore, tensor
+from synth import config
+
+RNG = np.random.default_rng(2010)
+
+
+def crand(*shape):
+    return RNG.standard_normal(shape) + 1j * RNG.standard_normal(shape)
+
+
+def orth(n, r):
+    q, _ = np.linalg.qr(crand(n, r))
+    return q
+
+
+# ---------------------------------------------------------------- tensor primitives
+def test_unfold_worked_example():
+    t = np.reshape(np.arange(1, 9), (2, 2, 2), order="F")      # data 1..8, first index fastest
+    np.testing.assert_array_equal(tensor.unfold(t, 2), [[1, 2, 5, 6], [3, 4, 7, 8]])
+    np.testing.assert_array_equal(tensor.unfold(t, 1), [[1, 3, 5, 7], [2, 4, 6, 8]])
+
+
+def test_fold_roundtrip_bit_exact():
+    t = crand(3, 4, 5, 2)
+    for m in range(1, 5):
+        assert np.array_equal(tensor.fold(tensor.unfold(t, m), m, t.shape), t)
+
+
+def test_mode_product_against_loops():
+    t = crand(2, 3, 4)
+    u = crand(5, 3)
+    y = tensor.mode_product(t, u, 2)
+    ref = np.zeros((2, 5, 4), complex)
+    for a in range(2):
+        for v in range(5):
+            for c in range(4):
+                ref[a, v, c] = sum(t[a, i, c] * u[v, i] for i in range(3))
+    np.testing.assert_allclose(y, ref, rtol=1e-14)
+    assert np.array_equal(tensor.mode_product(t, np.eye(3), 2), t)
+    a, b = crand(6, 2), crand(7, 3)
+    np.testing.assert_allclose(tensor.mode_product(tensor.mode_product(t, a, 1), b, 2),
+                               tensor.mode_product(tensor.mode_product(t, b, 2), a, 1), rtol=1e-13)
+
+
+def test_contract_mode3_against_loops():
+    x, y = crand(3, 3, 2), crand(2, 4, 2)
+    z = tensor.contract_mode3(x, y)
+    for a, b, c, d in np.ndindex(3, 3, 2, 4):
+        ref = x[a, b, 0] * y[c, d, 0] + x[a, b, 1] * y[c, d, 1]
+        assert abs(z[a, b, c, d] - ref) < 1e-13
+
+
+def test_rel_err_examples():
+    assert tensor.rel_err(np.array([3.0, 4.0]), np.array([0.0, 0.0])) == 1.0
+    assert abs(tensor.rel_err(np.array([3.0, 4.0]), np.array([3.0, 0.0])) - 0.8) < 1e-15
+
+
+# ---------------------------------------------------------------- truncation rule
+def test_tail_rank_examples():
+    assert decomp.tail_rank(np.array([1.0, 1e-3, 1e-9]), 1e-6).rank == 2
+    assert decomp.tail_rank(np.array([1.0, 1e-3, 1e-9]), 2e-3).rank == 1
+    assert decomp.tail_rank(np.array([3.0, 4.0]), 0.0).rank == 2
+    assert decomp.tail_rank(np.zeros(4), 0.0).rank == 1
+    # equality keeps the smaller rank
+    assert decomp.tail_rank(np.array([2.0, 1.0]), 1.0).rank == 1
+
+
+# ---------------------------------------------------------------- Alg. 1
+def test_tucker_recovers_known_multilinear_rank():
+    core = crand(3, 4, 5)
+    t = restore.tucker_full(core, [orth(9, 3), orth(8, 4), orth(10, 5)])
+    f = decomp.tucker_svd(t, 1e-8)
+    assert f.ranks == (3, 4, 5)
+    assert tensor.rel_err(t, restore.tucker_full(f.core, f.factors)) < 1e-12
+    for u in f.factors:
+        np.testing.assert_allclose(u.conj().T @ u, np.eye(u.shape[1]), atol=1e-10)
+
+
+def test_tucker_degenerate_inputs():
+    z = decomp.tucker_svd(np.zeros((4, 4, 4), complex), 1e-6)
+    assert z.ranks == (1, 1, 1) and np.all(z.core == 0)
+    a, b, c = crand(5), crand(6), crand(7)
+    t = np.einsum("i,j,k->ijk", a, b, c)
+    assert decomp.tucker_svd(t, 1e-6).ranks == (1, 1, 1)
+    assert decomp.tt_svd(t, 1e-6).ranks == (1, 1)
+    t4 = np.einsum("i,j,k,l->ijkl", a, b, c, crand(3))
+    assert decomp.htucker_svd(t4, 1e-6).ranks == (1, 1, 1, 1, 1, 1)
+
+
+@pytest.fixture(scope="module")
+def c1_ops():
+    c = config(1)
+    grid = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L)
+    khat, w, _, _ = fmm.direction_grid(c.L, c.nphi)
+    return fmm.fft_operator_4d(grid, khat)
+
+
+@pytest.mark.parametrize("gamma", [1e-2, 1e-4, 1e-6])
+def test_error_bounds_all_formats(c1_ops, gamma):
+    """||T - T_hat||_F <= gamma ||T||_F for every format (the per-step thresholds
+    make this a theorem)."""
+    T4 = c1_ops
+    for p in (0, 77, 200):
+        t = T4[..., p]
+        f = decomp.tucker_svd(t, gamma)
+        assert tensor.rel_err(t, restore.tucker_full(f.core, f.factors)) <= gamma
+        g = decomp.tt_svd(t, gamma)
+        assert tensor.rel_err(t, restore.tt3d_full(g.head, g.cores[0], g.tail)) <= gamma
+    f4 = decomp.tucker_svd(T4, gamma)
+    assert tensor.rel_err(T4, restore.tucker_full(f4.core, f4.factors)) <= gamma
+    h = decomp.htucker_svd(T4, gamma)
+    assert tensor.rel_err(T4, restore.htucker_full(h.leaves, h.c12, h.c34, h.c1234)) <= gamma
+    assert h.ranks[4] == h.ranks[5]                       # r12 = r34 (same singular values)
+    g4 = decomp.tt_svd(T4, gamma)
+    assert tensor.rel_err(T4, restore.tt4d_full(g4.head, g4.cores[0], g4.cores[1], g4.tail)) <= gamma
+
+
+def test_error_bound_is_not_vacuous(c1_ops):
+    """At a loose tolerance the truncation actually removes energy (the error is
+    within a factor ~sqrt(d) of gamma), so a dropped-term bug cannot hide."""
+    t = c1_ops[..., 40]
+    f = decomp.tucker_svd(t, 1e-1)
+    e = tensor.rel_err(t, restore.tucker_full(f.core, f.factors))
+    assert 1e-1 / 10 < e <= 1e-1
+
+
+def test_ranks_nonincreasing_in_gamma(c1_ops):
+    t = c1_ops[..., 123]
+    prev = None
+    for g in (1e-8, 1e-6, 1e-4, 1e-2, 1e-1):
+        r = decomp.tucker_svd(t, g).ranks
+        if prev is not None:
+            assert all(a <= b for a, b in zip(r, prev))
+        prev = r
+
+
+def test_tt_recovers_known_tt_ranks():
+    u1, c1, u3 = orth(6, 2), crand(2, 5, 3), orth(7, 3)
+    t = restore.tt3d_full(u1, c1, u3)
+    g = decomp.tt_svd(t, 1e-10)
+    assert g.ranks == (2, 3)
+    assert tensor.rel_err(t, restore.tt3d_full(g.head, g.cores[0], g.tail)) < 1e-12
+
+
+def test_htucker_recovers_known_ranks():
+    leaves = [orth(5, 2), orth(6, 3), orth(4, 2), orth(7, 3)]
+    c12, c34 = crand(2, 3, 2), crand(2, 3, 2)
+    root = crand(2, 2)
+    t = restore.htucker_full(leaves, c12, c34, root)
+    h = decomp.htucker_svd(t, 1e-10)
+    assert h.ranks == (2, 3, 2, 3, 2, 2)
+    assert tensor.rel_err(t, restore.htucker_full(h.leaves, h.c12, h.c34, h.c1234)) < 1e-12
+
+
+@pytest.mark.slow
+def test_table2_ranks(golden_dir):
+    """Table II, n = 32, 435 directions, gamma = 1e-6: the exact
+    direction-mode rank 225 = (L+1)^2 and the loose spatial ranks (max(10%, 3))."""
+    g = json.load(open(os.path.join(golden_dir, "table2.json")))
+    N = g["n"] // 2
+    grid = fmm.OperatorGrid(N, N, N, g["edge"], 2 * np.pi, g["L"])
+    khat, _, _, _ = fmm.direction_grid(g["L"], g["nphi"])
+    assert len(khat) == 435
+    T4 = fmm.fft_operator_4d(grid, khat)
+    tol = lambda ref: max(0.1 * ref, 3)
+    rmax = max(max(decomp.tucker_svd(T4[..., p], g["gamma"]).ranks) for p in range(0, 435, 6))
+    assert abs(rmax - g["tucker3d_rmax"]) <= tol(g["tucker3d_rmax"])
+    f = decomp.tucker_svd(T4, g["gamma"])
+    assert f.ranks[3] == g["tucker4d_r4"]
+    assert all(abs(r - g["tucker4d_r123"]) <= tol(g["tucker4d_r123"]) for r in f.ranks[:3])
