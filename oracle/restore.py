@@ -85,14 +85,22 @@ def tt3d_restore(u1, c1, u3) -> np.ndarray:
     return np.reshape(t1 @ u3.T, (n1, n2, n3), order="F")
 
 
-def tt4d_slice(u1, c1, c2, u4, p: int) -> np.ndarray:
+def tt4d_t2(c2, u4) -> np.ndarray:
+    """Fig. 4(b) step 1: T2 = C^2 (as r2 n3 x r3) times U^last transposed
+    (r2 n3 x n4).  Independent of p, so callers may compute it once."""
+    r2, n3, r3 = c2.shape
+    return np.reshape(c2, (r2 * n3, r3), order="F") @ u4.T
+
+
+def tt4d_slice(u1, c1, c2, u4, p: int, t2=None) -> np.ndarray:
     """Fig. 4(b): step 1 T2 = C^2 (as r2 n3 x r3) times U^last
     transposed; step 2 column p of T2, reshaped r2 x n3, left-multiplied by
     T1 (n1 n2 x r2) of Fig. 4(a) step 1; step 3 fold."""
     r1, n2, r2 = c1.shape
     _, n3, r3 = c2.shape
     n1 = u1.shape[0]
-    t2 = np.reshape(c2, (r2 * n3, r3), order="F") @ u4.T     # r2 n3 x n4
+    if t2 is None:
+        t2 = tt4d_t2(c2, u4)                                  # r2 n3 x n4
     col = np.reshape(t2[:, p], (r2, n3), order="F")
     t1 = np.reshape(u1 @ np.reshape(c1, (r1, n2 * r2), order="F"), (n1 * n2, r2), order="F")
     return np.reshape(t1 @ col, (n1, n2, n3), order="F")

@@ -1,0 +1,1035 @@
+// fmmt_api.cu -- C ABI of libfmmt: contexts, ops, and the translate hot path
+// (eq. (5) with on-the-fly restoration).
+//
+// Per matvec the op walks its directions in batches of PB (sized so the
+// batch's intermediates stay L2-resident) and launches, per batch:
+//   [a3]  direction-slice GEMMs (4D formats)              k_cgemm
+//   [a4]  restore chain up to G_p = (C_p x1 U1 x2 U2)      k_cgemm
+//   [a2]  pruned forward DFT along x, y                    k_fwd_xy
+//   [a4,a5,a2,a6] last restore contraction fused with the z-DFT, the Hadamard
+//         product and the truncated inverse z-DFT          k_conv_z
+//   [a6]  truncated inverse DFT along y, x, 1/n scaling    k_inv_xy
+// and, for translate_sum, the weighted direction sum (a7) + NCCL allreduce.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fmmt_internal.h"
+#include "kernels_fft.cuh"
+#include "kernels_gemm.cuh"
+
+using fmmt::GemmDesc;
+using fmmt::ZArgs;
+
+// ============================================================== errors
+namespace fmmt_internal {
+fmmt_status set_err(fmmt_ctx* ctx, fmmt_status st, const char* fmt, ...) {
+  if (ctx) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return st;
+}
+}  // namespace fmmt_internal
+using fmmt_internal::set_err;
+
+#define CHECK_ARG(ctx, cond, ...) \
+  do {                            \
+    if (!(cond)) return set_err((ctx), FMMT_E_ARG, __VA_ARGS__); \
+  } while (0)
+#define CHECK_SHAPE(ctx, cond, ...) \
+  do {                              \
+    if (!(cond)) return set_err((ctx), FMMT_E_SHAPE, __VA_ARGS__); \
+  } while (0)
+
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// ============================================================== profiling / launches
+static cudaEvent_t take_event(fmmt_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  fmmt_ctx* ctx;
+  const char* name;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(fmmt_ctx* c, const char* n) : ctx(c), name(n) {
+    ctx->launches++;
+    if (ctx->profiling) {
+      e0 = take_event(ctx);
+      cudaEventRecord(e0, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->profiling) {
+      cudaEvent_t e1 = take_event(ctx);
+      cudaEventRecord(e1, ctx->stream);
+      ctx->pending.push_back({name, e0, e1});
+    }
+  }
+};
+
+static void prof_flush(fmmt_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& pe : ctx->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pe.e0, pe.e1);
+    bool found = false;
+    for (auto& kv : ctx->prof)
+      if (strcmp(kv.first, pe.name) == 0) {
+        kv.second.first += ms;
+        kv.second.second += 1;
+        found = true;
+        break;
+      }
+    if (!found) ctx->prof.push_back({pe.name, {ms, 1}});
+    ctx->event_pool.push_back(pe.e0);
+    ctx->event_pool.push_back(pe.e1);
+  }
+  ctx->pending.clear();
+}
+
+// ============================================================== kernel dispatch
+namespace {
+
+struct XYKernels {
+  void (*fwd)(const float2*, float2*, int, int) = nullptr;
+  void (*inv)(const float2*, float2*, int, int, float) = nullptr;
+  int plane_smem = 0;     // complex elements per plane
+  int lines = 0;          // max concurrent line-items per plane (for planes-per-CTA)
+};
+
+template <int NX, int NY>
+XYKernels make_xy() {
+  using G = fmmt::XYGeom<NX, NY>;
+  using SX = fmmt::Split<NX>;
+  using SY = fmmt::Split<NY>;
+  XYKernels k;
+  k.fwd = fmmt::k_fwd_xy<NX, NY>;
+  k.inv = fmmt::k_inv_xy<NX, NY>;
+  k.plane_smem = G::PLANE_SMEM;
+  int lx = G::Ny * (SX::two_pass ? std::max(SX::A, SX::B) : 1);
+  int ly = NX * (SY::two_pass ? std::max(SY::A, SY::B) : 1);
+  k.lines = std::max(lx, ly);
+  return k;
+}
+
+template <int NX>
+XYKernels make_xy_ny(int ny) {
+  switch (ny) {
+    case 4: return make_xy<NX, 4>();
+    case 8: return make_xy<NX, 8>();
+    case 16: return make_xy<NX, 16>();
+    case 32: return make_xy<NX, 32>();
+    case 64: return make_xy<NX, 64>();
+    case 128: return make_xy<NX, 128>();
+    case 256: return make_xy<NX, 256>();
+  }
+  return XYKernels{};
+}
+
+XYKernels get_xy(int nx, int ny) {
+  switch (nx) {
+    case 4: return make_xy_ny<4>(ny);
+    case 8: return make_xy_ny<8>(ny);
+    case 16: return make_xy_ny<16>(ny);
+    case 32: return make_xy_ny<32>(ny);
+    case 64: return make_xy_ny<64>(ny);
+    case 128: return make_xy_ny<128>(ny);
+    case 256: return make_xy_ny<256>(ny);
+  }
+  return XYKernels{};
+}
+
+using ZFn = void (*)(ZArgs);
+struct ZKernel {
+  ZFn fn = nullptr;
+  int S = 1;
+};
+
+template <int N3>
+ZKernel make_z(int mode) {
+  constexpr int S = (N3 <= 32) ? 1 : 2;
+  ZKernel k;
+  k.S = S;
+  if (mode == fmmt::Z_DENSE) k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_DENSE>;
+  else if (mode == fmmt::Z_LOWRANK) k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_LOWRANK>;
+  else k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_RESTORE>;
+  return k;
+}
+
+ZKernel get_z(int n3, int mode) {
+  switch (n3) {
+    case 4: return make_z<4>(mode);
+    case 8: return make_z<8>(mode);
+    case 16: return make_z<16>(mode);
+    case 32: return make_z<32>(mode);
+    case 64: return make_z<64>(mode);
+  }
+  return ZKernel{};
+}
+
+}  // namespace
+
+// ============================================================== op
+struct GemmLaunch {
+  int first = 0;       // index into op->descs
+  int ndesc = 0;
+  int maxtiles = 0;    // for the chosen tile size
+  int maxsub = 0;
+  bool big = false;    // 64x64 tiles
+  const char* name = "";
+};
+
+struct Batch {
+  int q0 = 0, nq = 0;
+  std::vector<GemmLaunch> gemms;
+};
+
+struct fmmt_op {
+  fmmt_ctx* ctx = nullptr;
+  fmmt_format format = FMMT_DENSE;
+  int64_t n1 = 0, n2 = 0, n3 = 0, ndir = 0;
+  int nslots = 0;
+  std::vector<int64_t> ranks;                  // [ndir][nslots] (3D) or [nslots]
+  std::vector<float2*> arr;                    // device factor arrays (import order)
+  std::vector<int64_t> arr_elems;
+  std::vector<std::vector<int64_t>> off;       // per array, per direction offsets (3D formats)
+  int64_t* d_voff = nullptr;                   // per direction offset of the z-stage V factor
+  int* d_rank = nullptr;                       // per direction z-stage rank (3D formats)
+  float2* tbar1 = nullptr;                     // TT-4D: T1 = U1 . C1 (Fig. 4(a) step 1), n1 n2 x r2
+  // workspace
+  int64_t PB = 0;
+  float2 *W = nullptr, *H = nullptr, *Gw = nullptr, *Cw = nullptr, *Mw = nullptr, *Nw = nullptr,
+         *Vw = nullptr, *sigtmp = nullptr, *partial = nullptr;
+  int64_t ws_bytes = 0;
+  int64_t r2max = 1, r3max = 1, rGmax = 1;     // workspace rank bounds
+  std::vector<GemmDesc> descs;
+  GemmDesc* d_descs = nullptr;
+  std::vector<Batch> batches;
+  int nsplit = 1;
+  // host staging for translate_sum_host
+  float2* d_in_host = nullptr;   // device buffer for e2e input
+  float* d_w_host = nullptr;
+  float2* d_sum_host = nullptr;
+};
+
+static int64_t rk(const fmmt_op* op, int64_t p, int slot) {
+  if (op->format == FMMT_TUCKER3D || op->format == FMMT_TT3D) return op->ranks[p * op->nslots + slot];
+  return op->ranks[slot];
+}
+
+static void free_workspace(fmmt_op* op) {
+  float2** bufs[] = {&op->W, &op->H, &op->Gw, &op->Cw, &op->Mw, &op->Nw, &op->Vw, &op->sigtmp, &op->partial};
+  for (auto b : bufs) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  if (op->d_descs) cudaFree(op->d_descs);
+  op->d_descs = nullptr;
+  op->ws_bytes = 0;
+}
+
+void fmmt_op_destroy(fmmt_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->ctx->device);
+  cudaStreamSynchronize(op->ctx->stream);
+  free_workspace(op);
+  for (auto a : op->arr)
+    if (a) cudaFree(a);
+  if (op->d_voff) cudaFree(op->d_voff);
+  if (op->d_rank) cudaFree(op->d_rank);
+  if (op->tbar1) cudaFree(op->tbar1);
+  if (op->d_in_host) cudaFree(op->d_in_host);
+  if (op->d_w_host) cudaFree(op->d_w_host);
+  if (op->d_sum_host) cudaFree(op->d_sum_host);
+  delete op;
+}
+
+// per-direction workspace bytes for batch sizing
+static int64_t per_dir_ws(const fmmt_op* op) {
+  const int64_t n12 = op->n1 * op->n2, Nz = op->n3 / 2;
+  int64_t e = Nz * n12;   // W
+  switch (op->format) {
+    case FMMT_DENSE: break;
+    case FMMT_TUCKER3D: e += op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
+    case FMMT_TUCKER4D: e += rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) + op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
+    case FMMT_HTUCKER4D:
+      e += rk(op, 0, 2) * rk(op, 0, 5) + rk(op, 0, 4) * rk(op, 0, 2) + rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) +
+           op->n1 * op->r2max * op->r3max + n12 * op->r3max;
+      break;
+    case FMMT_TT3D: e += n12 * op->rGmax; break;
+    case FMMT_TT4D: e += rk(op, 0, 1) * op->n3; break;
+  }
+  return e * 8;
+}
+
+static fmmt_status cmalloc(fmmt_op* op, float2** p, int64_t elems) {
+  if (elems <= 0) elems = 1;
+  cudaError_t e = cudaMalloc(p, elems * sizeof(float2));
+  if (e != cudaSuccess) return set_err(op->ctx, FMMT_E_NOMEM, "cudaMalloc(%lld B) failed: %s", (long long)(elems * 8), cudaGetErrorString(e));
+  op->ws_bytes += elems * 8;
+  return FMMT_OK;
+}
+
+static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, const char* name) {
+  if (ds.empty()) return;
+  GemmLaunch L;
+  L.first = (int)op->descs.size();
+  L.ndesc = (int)ds.size();
+  L.name = name;
+  int64_t mmin = 1 << 30, nmin = 1 << 30;
+  for (auto& d : ds) {
+    mmin = std::min<int64_t>(mmin, d.m);
+    nmin = std::min<int64_t>(nmin, d.n);
+  }
+  L.big = (mmin >= 64 && nmin >= 64);
+  const int bm = L.big ? 64 : 32, bn = L.big ? 64 : 32;
+  for (auto& d : ds) {
+    int tiles = ((d.m + bm - 1) / bm) * ((d.n + bn - 1) / bn);
+    L.maxtiles = std::max(L.maxtiles, tiles);
+    L.maxsub = std::max(L.maxsub, d.batch);
+    op->descs.push_back(d);
+  }
+  b.gemms.push_back(L);
+}
+
+static GemmDesc gd(const float2* A, const float2* B, float2* C, int64_t m, int64_t n, int64_t k, int transB,
+                   int64_t lda, int64_t ldb, int64_t ldc, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+  GemmDesc d;
+  d.A = A; d.B = B; d.C = C;
+  d.m = (int)m; d.n = (int)n; d.k = (int)k;
+  d.transB = transB; d.batch = batch;
+  d.lda = lda; d.ldb = ldb; d.ldc = ldc;
+  d.sA = sA; d.sB = sB; d.sC = sC;
+  return d;
+}
+
+// Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
+// 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
+static void tucker_chain(fmmt_op* op, Batch& b) {
+  const int64_t n1 = op->n1, n2 = op->n2, n12 = n1 * n2;
+  std::vector<GemmDesc> sa, sb;
+  if (op->format == FMMT_TUCKER3D) {
+    for (int q = 0; q < b.nq; ++q) {
+      const int64_t p = b.q0 + q;
+      const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1), r3 = rk(op, p, 2);
+      const float2* core = op->arr[0] + op->off[0][p];
+      const float2* U1 = op->arr[1] + op->off[1][p];
+      const float2* U2 = op->arr[2] + op->off[2][p];
+      float2* Hq = op->H + q * n1 * op->r2max * op->r3max;
+      float2* Gq = op->Gw + q * n12 * op->rGmax;
+      sa.push_back(gd(U1, core, Hq, n1, r2 * r3, r1, 0, n1, r1, n1));
+      sb.push_back(gd(Hq, U2, Gq, n1, n2, r2, 1, n1, n2, n1, (int)r3, n1 * r2, 0, n12));
+    }
+  } else {
+    const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
+    const float2* U1 = op->arr[op->format == FMMT_TUCKER4D ? 1 : 0];
+    const float2* U2 = op->arr[op->format == FMMT_TUCKER4D ? 2 : 1];
+    sa.push_back(gd(U1, op->Cw, op->H, n1, r2 * r3, r1, 0, n1, r1, n1, b.nq, 0, r1 * r2 * r3, n1 * r2 * r3));
+    sb.push_back(gd(op->H, U2, op->Gw, n1, n2, r2, 1, n1, n2, n1, (int)(b.nq * r3), n1 * r2, 0, n12));
+  }
+  add_gemm(op, b, sa, "restore_mode1");
+  add_gemm(op, b, sb, "restore_mode2");
+}
+
+static fmmt_status build_plans(fmmt_op* op) {
+  free_workspace(op);
+  op->descs.clear();
+  op->batches.clear();
+  const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
+  if (op->PB <= 0) {
+    const int64_t target = 48ll << 20;
+    op->PB = std::max<int64_t>(1, std::min<int64_t>(op->ndir, target / std::max<int64_t>(1, per_dir_ws(op))));
+    // even batches
+    int64_t nb = (op->ndir + op->PB - 1) / op->PB;
+    op->PB = (op->ndir + nb - 1) / nb;
+  }
+  const int64_t PB = op->PB;
+  fmmt_status st;
+  if ((st = cmalloc(op, &op->W, PB * Nz * n12))) return st;
+  switch (op->format) {
+    case FMMT_DENSE: break;
+    case FMMT_TUCKER3D:
+      if ((st = cmalloc(op, &op->H, PB * n1 * op->r2max * op->r3max))) return st;
+      if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
+      break;
+    case FMMT_TUCKER4D:
+      if ((st = cmalloc(op, &op->Cw, PB * rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2)))) return st;
+      if ((st = cmalloc(op, &op->H, PB * n1 * op->r2max * op->r3max))) return st;
+      if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
+      break;
+    case FMMT_HTUCKER4D:
+      if ((st = cmalloc(op, &op->Mw, PB * rk(op, 0, 2) * rk(op, 0, 5)))) return st;
+      if ((st = cmalloc(op, &op->Nw, PB * rk(op, 0, 4) * rk(op, 0, 2)))) return st;
+      if ((st = cmalloc(op, &op->Cw, PB * rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2)))) return st;
+      if ((st = cmalloc(op, &op->H, PB * n1 * op->r2max * op->r3max))) return st;
+      if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
+      break;
+    case FMMT_TT3D:
+      if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
+      break;
+    case FMMT_TT4D:
+      if ((st = cmalloc(op, &op->Vw, PB * rk(op, 0, 1) * n3))) return st;
+      break;
+  }
+  for (int64_t q0 = 0; q0 < op->ndir; q0 += PB) {
+    Batch b;
+    b.q0 = (int)q0;
+    b.nq = (int)std::min<int64_t>(PB, op->ndir - q0);
+    switch (op->format) {
+      case FMMT_DENSE: break;
+      case FMMT_TUCKER3D: tucker_chain(op, b); break;
+      case FMMT_TUCKER4D: {
+        const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3);
+        // a3 (Fig. 3(b)): C_q = C(r1 r2 r3 x r4) . U4[p,:]^T
+        add_gemm(op, b, {gd(op->arr[0], op->arr[4] + b.q0, op->Cw, r1 * r2 * r3, b.nq, r4, 1, r1 * r2 * r3, op->ndir, r1 * r2 * r3)},
+                 "slice_tucker4d");
+        tucker_chain(op, b);
+        break;
+      }
+      case FMMT_HTUCKER4D: {
+        const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3), r12 = rk(op, 0, 4),
+                      r34 = rk(op, 0, 5);
+        const float2 *U4 = op->arr[3], *C12 = op->arr[4], *C34 = op->arr[5], *C1234 = op->arr[6];
+        // a3 (Fig. 3(c)): M_q[c,j] = sum_d C34[c,d,j] U4[p,d]
+        add_gemm(op, b, {gd(C34, U4 + b.q0, op->Mw, r3, b.nq, r4, 1, r3, op->ndir, r3 * r34, (int)r34, r3 * r4, 0, r3)},
+                 "slice_htucker_M");
+        // N_q = C1234 . M_q^T  (r12 x r3)
+        add_gemm(op, b, {gd(C1234, op->Mw, op->Nw, r12, r3, r34, 1, r12, r3, r12, b.nq, 0, r3 * r34, r12 * r3)},
+                 "slice_htucker_N");
+        // C_q = C12(r1 r2 x r12) . N_q  (r1 r2 x r3)
+        add_gemm(op, b, {gd(C12, op->Nw, op->Cw, r1 * r2, r3, r12, 0, r1 * r2, r12, r1 * r2, b.nq, 0, r12 * r3, r1 * r2 * r3)},
+                 "slice_htucker_C");
+        tucker_chain(op, b);
+        break;
+      }
+      case FMMT_TT3D: {
+        std::vector<GemmDesc> ds;
+        for (int q = 0; q < b.nq; ++q) {
+          const int64_t p = b.q0 + q;
+          const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1);
+          ds.push_back(gd(op->arr[0] + op->off[0][p], op->arr[1] + op->off[1][p], op->Gw + q * n12 * op->rGmax, n1,
+                          n2 * r2, r1, 0, n1, r1, n1));
+        }
+        add_gemm(op, b, ds, "restore_tt_head");
+        break;
+      }
+      case FMMT_TT4D: {
+        const int64_t r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
+        // a3 (Fig. 4(b) step 1, columns of T2 for the batch): V_q = C2(r2 n3 x r3) . U_last[p,:]^T
+        add_gemm(op, b, {gd(op->arr[2], op->arr[3] + b.q0, op->Vw, r2 * n3, b.nq, r3, 1, r2 * n3, op->ndir, r2 * n3)},
+                 "slice_tt4d");
+        break;
+      }
+    }
+    op->batches.push_back(b);
+  }
+  if (!op->descs.empty()) {
+    FMMT_CUDA(op->ctx, cudaMalloc(&op->d_descs, op->descs.size() * sizeof(GemmDesc)));
+    FMMT_CUDA(op->ctx, cudaMemcpy(op->d_descs, op->descs.data(), op->descs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+  }
+  return FMMT_OK;
+}
+
+// ============================================================== launches
+static fmmt_status launch_gemm(fmmt_op* op, const GemmLaunch& L) {
+  fmmt_ctx* ctx = op->ctx;
+  ProfScope ps(ctx, L.name);
+  dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
+  if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
+  if (L.big)
+    fmmt::k_cgemm<64, 64, 16, 4, 4><<<grid, 256, 0, ctx->stream>>>(op->d_descs + L.first);
+  else
+    fmmt::k_cgemm<32, 32, 16, 4, 4><<<grid, 64, 0, ctx->stream>>>(op->d_descs + L.first);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+static int xy_ppc(const XYKernels& k) {
+  int ppc = fmmt::XY_THREADS / std::max(1, k.lines);
+  ppc = std::max(1, std::min(16, ppc));
+  const int64_t cap = (220 << 10) / 8 - FMMT_TW_NMAX;
+  while (ppc > 1 && (int64_t)ppc * k.plane_smem > cap) --ppc;
+  return ppc;
+}
+
+static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* out, int nplanes, float scale) {
+  fmmt_ctx* ctx = op->ctx;
+  XYKernels k = get_xy((int)op->n1, (int)op->n2);
+  if (!k.fwd) return set_err(ctx, FMMT_E_UNSUPPORTED, "no xy kernel for n1=%lld n2=%lld", (long long)op->n1, (long long)op->n2);
+  const int ppc = xy_ppc(k);
+  const size_t smem = (size_t)(FMMT_TW_NMAX + (int64_t)ppc * k.plane_smem) * sizeof(float2);
+  const unsigned grid = (unsigned)((nplanes + ppc - 1) / ppc);
+  ProfScope ps(ctx, fwd ? "fft_fwd_xy" : "fft_inv_xy");
+  if (fwd) {
+    FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)k.fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k.fwd<<<grid, fmmt::XY_THREADS, smem, ctx->stream>>>(in, out, nplanes, ppc);
+  } else {
+    FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)k.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k.inv<<<grid, fmmt::XY_THREADS, smem, ctx->stream>>>(in, out, nplanes, ppc, scale);
+  }
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+static void fill_zargs(fmmt_op* op, ZArgs& a) {
+  const int64_t n12 = op->n1 * op->n2;
+  memset(&a, 0, sizeof(a));
+  a.n12 = n12;
+  switch (op->format) {
+    case FMMT_DENSE: a.T = op->arr[0]; break;
+    case FMMT_TUCKER3D:
+      a.G = op->Gw; a.g_stride = n12 * op->rGmax;
+      a.V = op->arr[3]; a.v_off = op->d_voff; a.v_sc = op->n3; a.v_sk = 1; a.rank_p = op->d_rank;
+      break;
+    case FMMT_TUCKER4D:
+      a.G = op->Gw; a.g_stride = n12 * rk(op, 0, 2);
+      a.V = op->arr[3]; a.v_stride = 0; a.v_sc = op->n3; a.v_sk = 1; a.rank = (int)rk(op, 0, 2);
+      break;
+    case FMMT_HTUCKER4D:
+      a.G = op->Gw; a.g_stride = n12 * rk(op, 0, 2);
+      a.V = op->arr[2]; a.v_stride = 0; a.v_sc = op->n3; a.v_sk = 1; a.rank = (int)rk(op, 0, 2);
+      break;
+    case FMMT_TT3D:
+      a.G = op->Gw; a.g_stride = n12 * op->rGmax;
+      a.V = op->arr[2]; a.v_off = op->d_voff; a.v_sc = op->n3; a.v_sk = 1; a.rank_p = op->d_rank;
+      break;
+    case FMMT_TT4D:
+      a.G = op->tbar1; a.g_stride = 0;
+      a.V = op->Vw; a.v_stride = rk(op, 0, 1) * op->n3; a.v_sc = 1; a.v_sk = rk(op, 0, 1); a.rank = (int)rk(op, 0, 1);
+      break;
+  }
+}
+
+static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout) {
+  fmmt_ctx* ctx = op->ctx;
+  ZKernel k = get_z((int)op->n3, mode);
+  if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
+  ZArgs a;
+  fill_zargs(op, a);
+  a.W = op->W + (int64_t)qoff * (op->n3 / 2) * a.n12;
+  a.p0 = p0;
+  a.G = a.G ? a.G + (int64_t)qoff * a.g_stride : nullptr;
+  if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
+  a.Tout = Tout;
+  const int lpc = fmmt::Z_THREADS / k.S;
+  dim3 grid((unsigned)((a.n12 + lpc - 1) / lpc), (unsigned)nq);
+  ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : (mode == fmmt::Z_DENSE ? "conv_z_dense" : "restore_conv_z"));
+  k.fn<<<grid, fmmt::Z_THREADS, 0, ctx->stream>>>(a);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
+  for (auto& L : b.gemms) {
+    fmmt_status st = launch_gemm(op, L);
+    if (st) return st;
+  }
+  return FMMT_OK;
+}
+
+static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out) {
+  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
+  const int Nz = (int)(op->n3 / 2);
+  const float scale = (float)(1.0 / ((double)op->n1 * (double)op->n2 * (double)op->n3));
+  const float2* in = reinterpret_cast<const float2*>(sig_in);
+  float2* out = reinterpret_cast<float2*>(sig_out);
+  for (const Batch& b : op->batches) {
+    fmmt_status st;
+    if ((st = run_batch_prep(op, b))) return st;
+    if ((st = launch_xy(op, true, in + (int64_t)b.q0 * K, op->W, b.nq * Nz, 1.f))) return st;
+    const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
+    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr))) return st;
+    if ((st = launch_xy(op, false, op->W, out + (int64_t)b.q0 * K, b.nq * Nz, scale))) return st;
+  }
+  return FMMT_OK;
+}
+
+static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void* out, int64_t ndir, int64_t Nx,
+                                        int64_t Ny, int64_t Nz) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, in && out, "null signature pointer");
+  CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
+  CHECK_SHAPE(ctx, 2 * Nx == op->n1 && 2 * Ny == op->n2 && 2 * Nz == op->n3, "grid %lldx%lldx%lld does not match op n=%lldx%lldx%lld",
+              (long long)Nx, (long long)Ny, (long long)Nz, (long long)op->n1, (long long)op->n2, (long long)op->n3);
+  const int64_t bytes = ndir * Nx * Ny * Nz * 8;
+  const char* a = (const char*)in;
+  const char* b = (const char*)out;
+  CHECK_ARG(ctx, a + bytes <= b || b + bytes <= a, "sig_in and sig_out overlap");
+  cudaPointerAttributes pa, pb;
+  if (cudaPointerGetAttributes(&pa, in) != cudaSuccess || cudaPointerGetAttributes(&pb, out) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, FMMT_E_ARG, "signature pointers are not CUDA device pointers");
+  }
+  CHECK_ARG(ctx, (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged) &&
+                     (pb.type == cudaMemoryTypeDevice || pb.type == cudaMemoryTypeManaged),
+            "signature pointers must be device memory");
+  if (pa.type == cudaMemoryTypeDevice && pa.device != ctx->device)
+    return set_err(ctx, FMMT_E_STATE, "sig_in is on device %d, context on %d", pa.device, ctx->device);
+  return FMMT_OK;
+}
+
+// ============================================================== C ABI
+extern "C" {
+
+int fmmt_version(void) { return FMMT_VERSION; }
+
+fmmt_status fmmt_init(int device, void* cuda_stream, fmmt_ctx** out) {
+  return fmmt_init_sharded(device, cuda_stream, 0, 1, nullptr, out);
+}
+
+fmmt_status fmmt_nccl_unique_id(void* out128) {
+  if (!out128) return FMMT_E_ARG;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return FMMT_E_NCCL;
+  memcpy(out128, &id, 128);
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world, const void* nccl_id, fmmt_ctx** out) {
+  if (!out) return FMMT_E_ARG;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return FMMT_E_ARG;
+  if (world > 1 && !nccl_id) return FMMT_E_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return FMMT_E_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return FMMT_E_CUDA;
+  fmmt_ctx* ctx = new fmmt_ctx();
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->rank = rank;
+  ctx->world = world;
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, 128);
+    ncclComm_t comm;
+    ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) {
+      delete ctx;
+      return FMMT_E_NCCL;
+    }
+    ctx->nccl_comm = comm;
+  }
+  *out = ctx;
+  return FMMT_OK;
+}
+
+void fmmt_destroy(fmmt_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& pe : ctx->pending) {
+    cudaEventDestroy(pe.e0);
+    cudaEventDestroy(pe.e1);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
+  fmmt_internal::setup_release(ctx);
+  delete ctx;
+}
+
+fmmt_status fmmt_sync(fmmt_ctx* ctx) {
+  if (!ctx) return FMMT_E_ARG;
+  cudaSetDevice(ctx->device);
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+const char* fmmt_last_error(const fmmt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fmmt_status fmmt_shard_range(int64_t ndir, int rank, int world, int64_t* begin, int64_t* count) {
+  if (!begin || !count || world < 1 || rank < 0 || rank >= world || ndir < 0) return FMMT_E_ARG;
+  const int64_t base = ndir / world, rem = ndir % world;
+  // the first `rem` ranks get one extra direction
+  *begin = rank * base + std::min<int64_t>(rank, rem);
+  *count = base + (rank < rem ? 1 : 0);
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_set_profiling(fmmt_ctx* ctx, int enable) {
+  if (!ctx) return FMMT_E_ARG;
+  ctx->profiling = enable != 0;
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_prof_reset(fmmt_ctx* ctx) {
+  if (!ctx) return FMMT_E_ARG;
+  prof_flush(ctx);
+  ctx->prof.clear();
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_t* launches, int64_t cap, int64_t* count) {
+  if (!ctx || !count) return FMMT_E_ARG;
+  prof_flush(ctx);
+  *count = (int64_t)ctx->prof.size();
+  for (int64_t i = 0; i < std::min<int64_t>(cap, *count); ++i) {
+    if (names) names[i] = ctx->prof[i].first;
+    if (ms) ms[i] = ctx->prof[i].second.first;
+    if (launches) launches[i] = ctx->prof[i].second.second;
+  }
+  return FMMT_OK;
+}
+
+int64_t fmmt_launch_count(const fmmt_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+fmmt_status fmmt_op_import(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
+                           const int64_t* ranks, const fmmt_c64* const* arrays, int64_t narrays, fmmt_op** op) {
+  return fmmt_internal::create_op(ctx, format, n1, n2, n3, ndir, ranks, (const void* const*)arrays, narrays, op);
+}
+
+fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
+  if (!op || !info) return FMMT_E_ARG;
+  memset(info, 0, sizeof(*info));
+  info->format = op->format;
+  info->n1 = op->n1; info->n2 = op->n2; info->n3 = op->n3; info->ndir = op->ndir;
+  info->nranks = op->nslots;
+  const bool per_dir = op->format == FMMT_TUCKER3D || op->format == FMMT_TT3D;
+  for (int s = 0; s < op->nslots; ++s) {
+    int64_t mx = 0;
+    double mean = 0;
+    const int64_t cnt = per_dir ? op->ndir : 1;
+    for (int64_t p = 0; p < cnt; ++p) {
+      int64_t r = rk(op, p, s);
+      mx = std::max(mx, r);
+      mean += (double)r;
+    }
+    info->rank_max[s] = mx;
+    info->rank_mean[s] = mean / (double)cnt;
+  }
+  int64_t comp = 0;
+  for (auto e : op->arr_elems) comp += e;
+  info->compressed_bytes = comp * 8;
+  info->original_bytes = op->n1 * op->n2 * op->n3 * op->ndir * 8;
+  info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0);
+  info->batch = op->PB;
+  // restore complex MACs per matvec (a3 + a4), in the contraction order the kernels use
+  const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n = n1 * n2 * n3;
+  double cm = 0;
+  for (int64_t p = 0; p < op->ndir; ++p) {
+    switch (op->format) {
+      case FMMT_DENSE: break;
+      case FMMT_TUCKER3D: case FMMT_TUCKER4D: case FMMT_HTUCKER4D: {
+        const double r1 = rk(op, p, 0), r2 = rk(op, p, 1), r3 = rk(op, p, 2);
+        cm += n1 * r1 * r2 * r3 + n1 * n2 * r2 * r3 + (double)n * r3;
+        if (op->format == FMMT_TUCKER4D) cm += r1 * r2 * r3 * rk(op, 0, 3);
+        if (op->format == FMMT_HTUCKER4D) {
+          const double r4 = rk(op, 0, 3), r12 = rk(op, 0, 4), r34 = rk(op, 0, 5);
+          cm += r3 * r4 * r34 + r12 * r34 * r3 + r1 * r2 * r12 * r3;
+        }
+        break;
+      }
+      case FMMT_TT3D: {
+        const double r1 = rk(op, p, 0), r2 = rk(op, p, 1);
+        cm += n1 * r1 * n2 * r2 + (double)n * r2;
+        break;
+      }
+      case FMMT_TT4D: {
+        const double r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
+        cm += r2 * n3 * r3 + (double)n * r2;
+        break;
+      }
+    }
+  }
+  info->restore_cmac = cm;
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_t* count) {
+  if (!op || !count) return FMMT_E_ARG;
+  *count = (int64_t)op->ranks.size();
+  if (ranks) {
+    if (cap < *count) return set_err(op->ctx, FMMT_E_ARG, "rank buffer too small (%lld < %lld)", (long long)cap, (long long)*count);
+    for (int64_t i = 0; i < *count; ++i) ranks[i] = op->ranks[i];
+  }
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs) {
+  if (!op || dirs < 0) return FMMT_E_ARG;
+  cudaSetDevice(op->ctx->device);
+  cudaStreamSynchronize(op->ctx->stream);
+  op->PB = std::min<int64_t>(dirs, op->ndir);
+  return build_plans(op);
+}
+
+fmmt_status fmmt_translate(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int64_t ndir, int64_t Nx, int64_t Ny,
+                           int64_t Nz) {
+  fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
+  if (st) return st;
+  cudaSetDevice(op->ctx->device);
+  return translate_impl(op, sig_in, sig_out);
+}
+
+static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float* w, float2* sum_out) {
+  fmmt_ctx* ctx = op->ctx;
+  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
+  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(op->ndir, std::max<int64_t>(1, (148 * 8 * 128) / std::max<int64_t>(K, 1))));
+  if (!op->partial || op->nsplit < nsplit) {
+    if (op->partial) cudaFree(op->partial);
+    op->partial = nullptr;
+    fmmt_status st = cmalloc(op, &op->partial, (int64_t)nsplit * K);
+    if (st) return st;
+    op->nsplit = nsplit;
+  }
+  {
+    ProfScope ps(ctx, "dirsum_partial");
+    dim3 grid((unsigned)((K + 127) / 128), (unsigned)nsplit);
+    fmmt::k_dirsum_partial<<<grid, 128, 0, ctx->stream>>>(sig, w, op->partial, K, (int)op->ndir, nsplit);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  {
+    ProfScope ps(ctx, "dirsum_final");
+    fmmt::k_dirsum_final<<<(unsigned)((K + 127) / 128), 128, 0, ctx->stream>>>(op->partial, sum_out, K, nsplit);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  if (ctx->world > 1) {
+    ncclResult_t r = ncclAllReduce(sum_out, sum_out, (size_t)(2 * K), ncclFloat, ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream);
+    if (r != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+  }
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_translate_sum(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, const float* w, fmmt_c64* sum_out,
+                               int64_t ndir, int64_t Nx, int64_t Ny, int64_t Nz) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, w && sum_out, "null weight or sum pointer");
+  cudaSetDevice(ctx->device);
+  const int64_t K = Nx * Ny * Nz;
+  if (!sig_out) {
+    if (!op->sigtmp) {
+      fmmt_status st = cmalloc(op, &op->sigtmp, op->ndir * (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2));
+      if (st) return st;
+    }
+    sig_out = reinterpret_cast<fmmt_c64*>(op->sigtmp);
+  }
+  fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
+  if (st) return st;
+  (void)K;
+  if ((st = translate_impl(op, sig_in, sig_out))) return st;
+  return dirsum_and_reduce(op, reinterpret_cast<const float2*>(sig_out), w, reinterpret_cast<float2*>(sum_out));
+}
+
+fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, const float* w_host, fmmt_c64* sum_out_host,
+                                    int64_t ndir, int64_t Nx, int64_t Ny, int64_t Nz) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, sig_in_host && w_host && sum_out_host, "null host pointer");
+  CHECK_SHAPE(ctx, ndir == op->ndir, "ndir mismatch");
+  cudaSetDevice(ctx->device);
+  const int64_t K = Nx * Ny * Nz;
+  if (!op->d_in_host) {
+    FMMT_CUDA(ctx, cudaMalloc(&op->d_in_host, ndir * K * sizeof(float2)));
+    FMMT_CUDA(ctx, cudaMalloc(&op->d_w_host, ndir * sizeof(float)));
+    FMMT_CUDA(ctx, cudaMalloc(&op->d_sum_host, K * sizeof(float2)));
+  }
+  FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_in_host, sig_in_host, ndir * K * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_w_host, w_host, ndir * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+  fmmt_status st = fmmt_translate_sum(op, reinterpret_cast<const fmmt_c64*>(op->d_in_host), nullptr, op->d_w_host,
+                                      reinterpret_cast<fmmt_c64*>(op->d_sum_host), ndir, Nx, Ny, Nz);
+  if (st) return st;
+  FMMT_CUDA(ctx, cudaMemcpyAsync(sum_out_host, op->d_sum_host, K * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, T_p, "null output");
+  CHECK_ARG(ctx, p >= 0 && p < op->ndir, "direction %lld out of range", (long long)p);
+  cudaSetDevice(ctx->device);
+  const int64_t n = op->n1 * op->n2 * op->n3;
+  if (op->format == FMMT_DENSE) {
+    ProfScope ps(ctx, "restore_copy");
+    FMMT_CUDA(ctx, cudaMemcpyAsync(T_p, op->arr[0] + p * n, n * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
+    return FMMT_OK;
+  }
+  for (const Batch& b : op->batches) {
+    if (p < b.q0 || p >= b.q0 + b.nq) continue;
+    fmmt_status st = run_batch_prep(op, b);
+    if (st) return st;
+    return launch_z(op, fmmt::Z_RESTORE, (int)p, (int)(p - b.q0), 1, reinterpret_cast<float2*>(T_p));
+  }
+  return set_err(ctx, FMMT_E_STATE, "no batch holds direction %lld", (long long)p);
+}
+
+}  // extern "C"
+
+// ============================================================== op creation
+namespace fmmt_internal {
+
+fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
+                      const int64_t* ranks, const void* const* arrays, int64_t narrays, fmmt_op** out) {
+  if (!ctx || !out) return FMMT_E_ARG;
+  *out = nullptr;
+  CHECK_ARG(ctx, format >= FMMT_DENSE && format <= FMMT_TT4D, "bad format %d", (int)format);
+  CHECK_ARG(ctx, arrays != nullptr, "null arrays");
+  CHECK_SHAPE(ctx, n1 >= 2 && n2 >= 2 && n3 >= 2 && ndir >= 1, "bad dims");
+  CHECK_SHAPE(ctx, n1 % 2 == 0 && n2 % 2 == 0 && n3 % 2 == 0, "n must be even (n = 2N)");
+  if (!(is_pow2(n1) && is_pow2(n2) && is_pow2(n3) && n1 >= 4 && n2 >= 4 && n3 >= 4 && n1 <= 256 && n2 <= 256 && n3 <= 64))
+    return set_err(ctx, FMMT_E_UNSUPPORTED, "translate path supports power-of-two n1,n2 in [4,256], n3 in [4,64]; got %lldx%lldx%lld",
+                   (long long)n1, (long long)n2, (long long)n3);
+  static const int nslots_of[] = {0, 3, 4, 6, 2, 3};
+  static const int narr_of[] = {1, 4, 5, 7, 3, 4};
+  CHECK_ARG(ctx, narrays == narr_of[format], "format %d needs %d arrays, got %lld", (int)format, narr_of[format], (long long)narrays);
+  for (int i = 0; i < narr_of[format]; ++i) CHECK_ARG(ctx, arrays[i] != nullptr, "array %d is null", i);
+  cudaSetDevice(ctx->device);
+  fmmt_op* op = new fmmt_op();
+  op->ctx = ctx;
+  op->format = format;
+  op->n1 = n1; op->n2 = n2; op->n3 = n3; op->ndir = ndir;
+  op->nslots = nslots_of[format];
+  const bool per_dir = format == FMMT_TUCKER3D || format == FMMT_TT3D;
+  if (op->nslots) {
+    CHECK_ARG(ctx, ranks != nullptr, "null ranks");
+    const int64_t cnt = per_dir ? ndir * op->nslots : op->nslots;
+    op->ranks.assign(ranks, ranks + cnt);
+    for (auto r : op->ranks)
+      if (r < 1) {
+        delete op;
+        return set_err(ctx, FMMT_E_SHAPE, "ranks must be >= 1");
+      }
+  }
+  // element counts per array (and per-direction offsets for 3D formats)
+  std::vector<int64_t> elems;
+  op->off.clear();
+  auto R = [&](int64_t p, int s) { return rk(op, p, s); };
+  switch (format) {
+    case FMMT_DENSE: elems = {n1 * n2 * n3 * ndir}; break;
+    case FMMT_TUCKER3D: {
+      op->off.assign(4, std::vector<int64_t>(ndir));
+      elems.assign(4, 0);
+      for (int64_t p = 0; p < ndir; ++p) {
+        const int64_t r1 = R(p, 0), r2 = R(p, 1), r3 = R(p, 2);
+        if (r1 > n1 || r2 > n2 || r3 > n3) { delete op; return set_err(ctx, FMMT_E_SHAPE, "rank exceeds mode size"); }
+        const int64_t sz[4] = {r1 * r2 * r3, n1 * r1, n2 * r2, n3 * r3};
+        for (int i = 0; i < 4; ++i) { op->off[i][p] = elems[i]; elems[i] += sz[i]; }
+        op->r2max = std::max(op->r2max, r2);
+        op->r3max = std::max(op->r3max, r3);
+      }
+      op->rGmax = op->r3max;
+      break;
+    }
+    case FMMT_TUCKER4D: {
+      const int64_t r1 = R(0, 0), r2 = R(0, 1), r3 = R(0, 2), r4 = R(0, 3);
+      elems = {r1 * r2 * r3 * r4, n1 * r1, n2 * r2, n3 * r3, ndir * r4};
+      op->r2max = r2; op->r3max = r3; op->rGmax = r3;
+      break;
+    }
+    case FMMT_HTUCKER4D: {
+      const int64_t r1 = R(0, 0), r2 = R(0, 1), r3 = R(0, 2), r4 = R(0, 3), r12 = R(0, 4), r34 = R(0, 5);
+      elems = {n1 * r1, n2 * r2, n3 * r3, ndir * r4, r1 * r2 * r12, r3 * r4 * r34, r12 * r34};
+      op->r2max = r2; op->r3max = r3; op->rGmax = r3;
+      break;
+    }
+    case FMMT_TT3D: {
+      op->off.assign(3, std::vector<int64_t>(ndir));
+      elems.assign(3, 0);
+      for (int64_t p = 0; p < ndir; ++p) {
+        const int64_t r1 = R(p, 0), r2 = R(p, 1);
+        const int64_t sz[3] = {n1 * r1, r1 * n2 * r2, n3 * r2};
+        for (int i = 0; i < 3; ++i) { op->off[i][p] = elems[i]; elems[i] += sz[i]; }
+        op->rGmax = std::max(op->rGmax, r2);
+      }
+      break;
+    }
+    case FMMT_TT4D: {
+      const int64_t r1 = R(0, 0), r2 = R(0, 1), r3 = R(0, 2);
+      elems = {n1 * r1, r1 * n2 * r2, r2 * n3 * r3, ndir * r3};
+      break;
+    }
+  }
+  op->arr_elems = elems;
+  for (size_t i = 0; i < elems.size(); ++i) {
+    float2* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, std::max<int64_t>(1, elems[i]) * sizeof(float2));
+    if (e != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_NOMEM, "factor allocation failed: %s", cudaGetErrorString(e));
+    }
+    op->arr.push_back(d);
+    e = cudaMemcpy(d, arrays[i], elems[i] * sizeof(float2), cudaMemcpyDefault);
+    if (e != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_CUDA, "factor copy failed: %s", cudaGetErrorString(e));
+    }
+  }
+  if (per_dir) {
+    // z-stage V factor offsets and ranks per direction
+    std::vector<int64_t> voff(ndir);
+    std::vector<int> rz(ndir);
+    const int vi = (format == FMMT_TUCKER3D) ? 3 : 2;
+    for (int64_t p = 0; p < ndir; ++p) {
+      voff[p] = op->off[vi][p];
+      rz[p] = (int)(format == FMMT_TUCKER3D ? R(p, 2) : R(p, 1));
+    }
+    cudaMalloc(&op->d_voff, ndir * sizeof(int64_t));
+    cudaMalloc(&op->d_rank, ndir * sizeof(int));
+    cudaMemcpy(op->d_voff, voff.data(), ndir * sizeof(int64_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(op->d_rank, rz.data(), ndir * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  fmmt_status st = build_plans(op);
+  if (st) {
+    fmmt_op_destroy(op);
+    return st;
+  }
+  if (format == FMMT_TT4D) {
+    // T1 = U1 . C1 (Fig. 4(a) step 1, reused by every direction of Fig. 4(b)), stored [b][ij]
+    const int64_t r1 = R(0, 0), r2 = R(0, 1);
+    if (cudaMalloc(&op->tbar1, n1 * n2 * r2 * sizeof(float2)) != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_NOMEM, "T1 allocation failed");
+    }
+    Batch tmp;
+    const size_t first = op->descs.size();
+    add_gemm(op, tmp, {gd(op->arr[0], op->arr[1], op->tbar1, n1, n2 * r2, r1, 0, n1, r1, n1)}, "tt4d_T1");
+    GemmDesc* dd = nullptr;
+    cudaMalloc(&dd, sizeof(GemmDesc));
+    cudaMemcpy(dd, &op->descs[first], sizeof(GemmDesc), cudaMemcpyHostToDevice);
+    GemmLaunch L = tmp.gemms[0];
+    const int bm = L.big ? 64 : 32;
+    (void)bm;
+    dim3 grid((unsigned)L.maxtiles, 1, 1);
+    if (L.big) fmmt::k_cgemm<64, 64, 16, 4, 4><<<grid, 256, 0, ctx->stream>>>(dd);
+    else fmmt::k_cgemm<32, 32, 16, 4, 4><<<grid, 64, 0, ctx->stream>>>(dd);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(dd);
+    op->descs.resize(first);
+    if (e != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_CUDA, "T1 gemm failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = op;
+  return FMMT_OK;
+}
+
+}  // namespace fmmt_internal

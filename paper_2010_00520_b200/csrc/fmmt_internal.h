@@ -1,0 +1,53 @@
+// fmmt_internal.h -- library-private structures shared by the translation
+// units of libfmmt (fmmt_api.cu: hot path + op management; fmmt_setup.cu:
+// direction grid, FP64 operator builder, FP64 compressor).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/fmmt.h"
+
+struct fmmt_prof_entry {
+  const char* name;
+  cudaEvent_t e0, e1;
+};
+
+struct fmmt_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  void* nccl_comm = nullptr;        // ncclComm_t when world > 1
+  std::string err;
+  int64_t launches = 0;
+  bool profiling = false;
+  std::vector<fmmt_prof_entry> pending;
+  std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
+  std::vector<cudaEvent_t> event_pool;
+  void* blas = nullptr;             // cublasHandle_t (setup only)
+  void* solver = nullptr;           // cusolverDnHandle_t (setup only)
+};
+
+namespace fmmt_internal {
+
+fmmt_status set_err(fmmt_ctx* ctx, fmmt_status st, const char* fmt, ...);
+
+// Create an op from complex64 arrays (host or device memory, copied).
+fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3,
+                      int64_t ndir, const int64_t* ranks, const void* const* arrays,
+                      int64_t narrays, fmmt_op** out);
+
+void setup_release(fmmt_ctx* ctx);   // free cuBLAS / cuSOLVER handles
+
+}  // namespace fmmt_internal
+
+#define FMMT_CUDA(ctx, call)                                                                \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fmmt_internal::set_err((ctx), FMMT_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, \
+                                    #call, cudaGetErrorString(e_));                        \
+  } while (0)

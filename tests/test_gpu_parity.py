@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA library (through its C ABI) vs the FP64 oracle on
+identical seeded inputs and identical (oracle-computed, complex64-rounded)
+compressed factors.
+
+Bars (BASELINE.json north_star):
+  * restored operator   ||T_gpu - T_oracle||_F / ||T_oracle||_F <= 1e-6 per direction,
+  * translate           per-direction relative L2 <= 1e-5 (complex64),
+  * compression ranks   identical integers (up to the tie rule of DESIGN.md Q18),
+  * GPU-built operator  matches the oracle's eq. (7) + FFT to 1e-11 (FP64).
+"""
+import numpy as np
+import pytest
+
+from oracle import decomp, fmm, restore, tensor, translate
+from synth import config, signature_seed, signatures
+
+from tests._helpers import Compressed, operator, rel, t_lib_to_math
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TRANSLATE_TOL = 1e-5
+RESTORE_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def fm():
+    from paper_2010_00520_b200 import build
+    build.build()
+    from paper_2010_00520_b200 import fmmt
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return fmmt
+
+
+@pytest.fixture(scope="module")
+def ctx(fm):
+    c = fm.Context(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_translate(fm, ctx, op, sig, N):
+    d_in = dev(sig)
+    d_out = torch.empty_like(d_in)
+    op.translate(d_in, d_out, sig.shape[0], N)
+    ctx.sync()
+    return d_out.cpu().numpy()
+
+
+# cache oracle compressions per (cfg, fmt, tol, ndir)
+_CACHE = {}
+
+
+def compressed(cfg, fmt, tol, ndir=None):
+    key = (cfg, fmt, tol, ndir)
+    if key not in _CACHE:
+        T4, w, _ = operator(cfg, ndir)
+        _CACHE[key] = Compressed(fmt, T4, tol)
+    return _CACHE[key]
+
+
+CASES = [
+    (1, "dense", 0.0), (1, "tucker3d", 1e-4), (1, "tt3d", 1e-4), (1, "tucker4d", 1e-4),
+    (1, "htucker4d", 1e-4), (1, "tt4d", 1e-4),
+    (2, "dense", 0.0), (2, "tucker3d", 1e-4), (2, "tt3d", 1e-4), (2, "tucker4d", 1e-4),
+    (2, "htucker4d", 1e-4), (2, "tt4d", 1e-4),
+    (2, "tucker3d", 1e-6), (2, "tt3d", 1e-6), (2, "tucker4d", 1e-6), (2, "htucker4d", 1e-6), (2, "tt4d", 1e-6),
+]
+
+
+@pytest.mark.parametrize("cfg,fmt,tol", CASES)
+def test_restore_parity(fm, ctx, cfg, fmt, tol):
+    cp = compressed(cfg, fmt, tol)
+    op = ctx.import_op(fmt, cp.n, cp.ndir, cp.ranks, cp.arrays)
+    out = torch.empty(int(np.prod(cp.n)), dtype=torch.complex64, device="cuda")
+    worst = 0.0
+    for p in sorted({0, 1, cp.ndir // 3, cp.ndir // 2, cp.ndir - 1}):
+        op.restore(p, out)
+        ctx.sync()
+        got = t_lib_to_math(out.cpu().numpy(), cp.n)
+        worst = max(worst, rel(cp.restore(p), got))
+    op.close()
+    assert worst <= RESTORE_TOL, worst
+
+
+@pytest.mark.parametrize("cfg,fmt,tol", CASES)
+def test_translate_parity(fm, ctx, cfg, fmt, tol):
+    c = config(cfg)
+    cp = compressed(cfg, fmt, tol)
+    op = ctx.import_op(fmt, cp.n, cp.ndir, cp.ranks, cp.arrays)
+    sig = signatures(signature_seed(cfg, 0), cp.ndir, c.Nx, c.Ny, c.Nz)
+    out = run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+    op.close()
+    sm, om = translate.sig_to_math(sig), translate.sig_to_math(out)
+    errs = [rel(cp.translate(sm, p), om[p]) for p in range(cp.ndir)]
+    assert max(errs) <= TRANSLATE_TOL, (max(errs), int(np.argmax(errs)))
+
+
+@pytest.mark.parametrize("fmt,tol", [("tucker3d", 1e-5), ("tt3d", 1e-5), ("dense", 0.0)])
+def test_translate_parity_config3_elongated(fm, ctx, fmt, tol):
+    """Config 3 (128x8x8 boxes, 256x16x16 grid): two-pass x-FFT, n3 = 16.
+    First 48 directions (the oracle's compression is the slow part)."""
+    c = config(3)
+    cp = compressed(3, fmt, tol, 48)
+    op = ctx.import_op(fmt, cp.n, cp.ndir, cp.ranks, cp.arrays)
+    sig = signatures(signature_seed(3, 0), cp.ndir, c.Nx, c.Ny, c.Nz)
+    out = run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+    op.close()
+    sm, om = translate.sig_to_math(sig), translate.sig_to_math(out)
+    errs = [rel(cp.translate(sm, p), om[p]) for p in range(cp.ndir)]
+    assert max(errs) <= TRANSLATE_TOL, max(errs)
+
+
+@pytest.mark.parametrize("N", [(2, 2, 2), (4, 2, 8), (8, 16, 4), (32, 4, 2), (64, 64, 32), (128, 2, 4), (2, 128, 32)])
+def test_translate_shapes_dense_random(fm, ctx, N):
+    """Every FFT path (single pass <= 32, four-step 64..256, z split S = 2 at
+    n3 = 64) on random operators, ragged direction counts, vs the oracle's
+    FP64 FFT path and, on small grids, the O(N^2) direct sum."""
+    rng = np.random.default_rng(sum(N))
+    n = tuple(2 * x for x in N)
+    nd = 3
+    T = (rng.standard_normal(n + (nd,)) + 1j * rng.standard_normal(n + (nd,))).astype(np.complex64)
+    op = ctx.import_op("dense", n, nd, None, [T.ravel(order="F")])
+    sig = signatures(17 + sum(N), nd, *N)
+    out = run_translate(fm, ctx, op, sig, N)
+    op.close()
+    sm, om = translate.sig_to_math(sig), translate.sig_to_math(out)
+    for p in range(nd):
+        ref = translate.translate_fft(T[..., p].astype(np.complex128), sm[p])
+        assert rel(ref, om[p]) <= TRANSLATE_TOL
+        if np.prod(N) <= 64:
+            d = translate.translate_direct(translate.spatial_kernel(T[..., p].astype(np.complex128)), sm[p])
+            assert rel(d, om[p]) <= TRANSLATE_TOL
+
+
+def test_translate_sum_and_host_e2e(fm, ctx):
+    c = config(2)
+    cp = compressed(2, "tucker3d", 1e-4)
+    op = ctx.import_op("tucker3d", cp.n, cp.ndir, cp.ranks, cp.arrays)
+    _, w, _ = operator(2)
+    sig = signatures(signature_seed(2, 1), cp.ndir, c.Nx, c.Ny, c.Nz)
+    N = (c.Nx, c.Ny, c.Nz)
+    d_in = dev(sig)
+    d_out = torch.empty_like(d_in)
+    d_w = dev(w.astype(np.float32))
+    d_sum = torch.empty((c.Nz, c.Ny, c.Nx), dtype=torch.complex64, device="cuda")
+    op.translate_sum(d_in, d_out, d_w, d_sum, cp.ndir, N)
+    ctx.sync()
+    sm = translate.sig_to_math(sig)
+    B = np.stack([cp.translate(sm, p) for p in range(cp.ndir)])
+    ref = translate.direction_sum(B, w.astype(np.float32).astype(np.float64))
+    got = np.transpose(d_sum.cpu().numpy(), (2, 1, 0))
+    assert rel(ref, got) <= TRANSLATE_TOL
+    # sig_out = NULL path and the host-buffer end-to-end call give the same sum
+    d_sum2 = torch.empty_like(d_sum)
+    op.translate_sum(d_in, None, d_w, d_sum2, cp.ndir, N)
+    ctx.sync()
+    assert torch.equal(d_sum2, d_sum)
+    host_out = np.zeros((c.Nz, c.Ny, c.Nx), dtype=np.complex64)
+    op.translate_sum_host(sig, w.astype(np.float32), host_out, cp.ndir, N)
+    assert np.array_equal(host_out, d_sum.cpu().numpy())
+    # virtual sharding: the sum over 2 shards equals the unsharded sum (fp32 order)
+    half = cp.ndir // 2
+    parts = []
+    for lo, hi in ((0, half), (half, cp.ndir)):
+        arrays = [None] * 4
+        rk = cp.ranks[lo:hi]
+        arrays[0] = np.concatenate([a.ravel(order="F").astype(np.complex64) for a in cp.cores[lo:hi]])
+        for i in range(3):
+            arrays[i + 1] = np.concatenate([u[i].ravel(order="F").astype(np.complex64) for u in cp.U[lo:hi]])
+        sop = ctx.import_op("tucker3d", cp.n, hi - lo, rk, arrays)
+        s = torch.empty_like(d_sum)
+        sop.translate_sum(d_in[lo:hi].contiguous(), None, d_w[lo:hi].contiguous(), s, hi - lo, N)
+        ctx.sync()
+        parts.append(s.cpu().numpy())
+        sop.close()
+    assert rel(d_sum.cpu().numpy(), parts[0] + parts[1]) <= 1e-6
+    op.close()
+
+
+def test_gpu_operator_builder_matches_oracle(fm, ctx):
+    for cfg, nd in ((1, 338), (2, 40), (3, 12)):
+        c = config(cfg)
+        khat, _ = fm.direction_grid(c.L, c.nphi)
+        khat = khat[:nd]
+        n = c.n
+        T = torch.empty((nd,) + n[::-1], dtype=torch.complex128, device="cuda")
+        ctx.build_operator(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L, khat, T)
+        ctx.sync()
+        got = T.cpu().numpy()
+        ok, _, _, _ = fmm.direction_grid(c.L, c.nphi)
+        grid = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L)
+        for p in sorted({0, nd // 2, nd - 1}):
+            ref = fmm.fft_operator_3d(grid, ok[p])
+            assert rel(ref, np.transpose(got[p], (2, 1, 0))) < 1e-11
+
+
+def _rank_ok(gpu_r, ora_trunc):
+    """Identical ranks, except within the tie band (margin < 1e-9) of Q18."""
+    for g, tr in zip(gpu_r, ora_trunc):
+        if g != tr.rank:
+            if not (tr.margin < 1e-9 and abs(g - tr.rank) == 1):
+                return False
+    return True
+
+
+@pytest.mark.parametrize("fmt,tol", [("tucker3d", 1e-4), ("tt3d", 1e-4), ("tucker4d", 1e-4), ("htucker4d", 1e-4),
+                                     ("tt4d", 1e-4), ("tucker3d", 1e-6), ("tucker4d", 1e-6), ("htucker4d", 1e-6),
+                                     ("tt4d", 1e-6), ("tt3d", 1e-6), ("dense", 0.5)])
+def test_gpu_compress_ranks_and_error(fm, ctx, fmt, tol):
+    """GPU FP64 compressor on the oracle's T (config 2, complex128 host input):
+    integer ranks identical to the oracle's Alg. 1/2/3, and the GPU restore of
+    the GPU factors within the truncation bound of the oracle's T."""
+    c = config(2)
+    T4, _, _ = operator(2)
+    nd = T4.shape[3]
+    Tlib = np.ascontiguousarray(np.transpose(T4, (3, 2, 1, 0)))      # [p][k][j][i]
+    op = ctx.compress(Tlib, c.n, nd, fmt, tol)
+    ranks = op.ranks()
+    if fmt in ("tucker3d", "tt3d"):
+        ranks = ranks.reshape(nd, -1)
+        for p in range(0, nd, 13):
+            o = decomp.tucker_svd(T4[..., p], tol) if fmt == "tucker3d" else decomp.tt_svd(T4[..., p], tol)
+            assert _rank_ok(ranks[p], o.truncations), (p, ranks[p], o.ranks)
+    elif fmt == "tucker4d":
+        o = decomp.tucker_svd(T4, tol)
+        assert _rank_ok(ranks, o.truncations), (ranks, o.ranks)
+    elif fmt == "htucker4d":
+        o = decomp.htucker_svd(T4, tol)
+        assert _rank_ok(ranks, o.truncations), (ranks, o.ranks)
+    elif fmt == "tt4d":
+        o = decomp.tt_svd(T4, tol)
+        assert _rank_ok(ranks, o.truncations), (ranks, o.ranks)
+    # restored-operator error of the GPU's own factors vs the oracle's T
+    out = torch.empty(int(np.prod(c.n)), dtype=torch.complex64, device="cuda")
+    num = den = 0.0
+    for p in range(0, nd, 11):
+        op.restore(p, out)
+        ctx.sync()
+        got = t_lib_to_math(out.cpu().numpy(), c.n)
+        num += np.linalg.norm((got - T4[..., p]).ravel()) ** 2
+        den += np.linalg.norm(T4[..., p].ravel()) ** 2
+        if fmt in ("tucker3d", "tt3d"):
+            # per-direction bound (3D formats compress each slice to tol) + complex64 floor
+            assert rel(T4[..., p], got) <= tol * (1 + 1e-3) + 2e-6
+    if fmt == "dense":
+        assert np.sqrt(num / den) < 1e-6
+    else:
+        # 4D formats bound the global error; the sampled-slice aggregate is
+        # checked against 2 tol (+ complex64 floor), Q16
+        assert np.sqrt(num / den) <= 2 * tol + 2e-6
+    op.close()
+
+
+def test_error_codes(fm, ctx):
+    c = config(1)
+    cp = compressed(1, "dense", 0.0)
+    op = ctx.import_op("dense", cp.n, cp.ndir, None, cp.arrays)
+    sig = signatures(1, cp.ndir, c.Nx, c.Ny, c.Nz)
+    d_in = dev(sig)
+    d_out = torch.empty_like(d_in)
+    with pytest.raises(fm.FmmtError, match="E_SHAPE"):
+        op.translate(d_in, d_out, cp.ndir - 1, (c.Nx, c.Ny, c.Nz))
+    with pytest.raises(fm.FmmtError, match="E_SHAPE"):
+        op.translate(d_in, d_out, cp.ndir, (c.Nx, c.Ny, 2 * c.Nz))
+    with pytest.raises(fm.FmmtError, match="E_ARG"):
+        op.translate(d_in, d_in, cp.ndir, (c.Nx, c.Ny, c.Nz))            # aliasing
+    with pytest.raises(fm.FmmtError, match="E_ARG"):
+        op.translate(sig, d_out, cp.ndir, (c.Nx, c.Ny, c.Nz))            # host pointer
+    with pytest.raises(fm.FmmtError, match="E_UNSUPPORTED"):
+        ctx.import_op("dense", (12, 8, 8), 1, None, [np.zeros(12 * 64, np.complex64)])
+    with pytest.raises(fm.FmmtError, match="E_ARG"):
+        ctx.compress(np.zeros((1, 8, 8, 8), np.complex128), (8, 8, 8), 1, "tucker3d", 1.5)
+    with pytest.raises(fm.FmmtError, match="E_SHAPE"):
+        ctx.import_op("tucker3d", (8, 8, 8), 1, [[9, 1, 1]], [np.zeros(9, np.complex64)] * 4)
+    op.close()
+
+
+def test_single_direction_and_batching_invariance(fm, ctx):
+    """ndir = 1 and every batch size give bit-identical outputs (the batch
+    split only changes which directions share a launch)."""
+    c = config(2)
+    cp = compressed(2, "tucker4d", 1e-4)
+    sig = signatures(signature_seed(2, 3), cp.ndir, c.Nx, c.Ny, c.Nz)
+    op = ctx.import_op("tucker4d", cp.n, cp.ndir, cp.ranks, cp.arrays)
+    ref = run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+    for b in (1, 7, 338):
+        op.set_batch(b)
+        assert np.array_equal(run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz)), ref)
+    op.close()
+    # single direction (U4 row subset)
+    arrays = list(cp.arrays)
+    U4 = cp.U[3][5:6]
+    arrays[4] = U4.ravel(order="F").astype(np.complex64)
+    op1 = ctx.import_op("tucker4d", cp.n, 1, cp.ranks, arrays)
+    out1 = run_translate(fm, ctx, op1, sig[5:6], (c.Nx, c.Ny, c.Nz))
+    op1.close()
+    sm = translate.sig_to_math(sig)
+    assert rel(cp.translate(sm, 5), translate.sig_to_math(out1)[0]) <= TRANSLATE_TOL
