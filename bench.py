@@ -64,7 +64,7 @@ def kernel_work(info: dict, fmt: str, ranks: np.ndarray, ndir: int):
         rr = ranks.reshape(ndir, -1).astype(np.float64)
     else:
         rr = np.tile(ranks.astype(np.float64), (ndir, 1))
-    if fmt in ("tucker3d", "tucker4d", "htucker4d"):
+    if fmt in ("tucker3d", "tucker4d"):
         r1, r2, r3 = rr[:, 0], rr[:, 1], rr[:, 2]
         w["restore_mode1"] = 8 * float(np.sum(n1 * r1 * r2 * r3))
         w["restore_mode2"] = 8 * float(np.sum(n12 * r2 * r3))
@@ -82,8 +82,8 @@ def kernel_work(info: dict, fmt: str, ranks: np.ndarray, ndir: int):
     if fmt == "htucker4d":
         r1, r2, r3, r4, r12, r34 = [rr[:, i] for i in range(6)]
         w["slice_htucker_M"] = 8 * float(np.sum(r3 * r4 * r34))
-        w["slice_htucker_N"] = 8 * float(np.sum(r12 * r34 * r3))
-        w["slice_htucker_C"] = 8 * float(np.sum(r1 * r2 * r12 * r3))
+        w["slice_htucker_G"] = 8 * float(np.sum(n12 * r34 * r3))
+        rz = r3
     if fmt == "dense":
         w["conv_z_dense"] = float(ndir * n * 8)           # bytes: the operator read once
     else:
@@ -177,6 +177,7 @@ def run_ours(args):
     else:
         ctx = fmmt.Context(local, stream.cuda_stream)
     d0, dn = fmmt.shard_range(ndir, rank, world)
+    ctx.set_gemm_impl(args.gemm)
 
     # setup (untimed): directions, FP64 operator on the GPU, GPU compression
     t_setup = time.time()
@@ -186,7 +187,11 @@ def run_ours(args):
         ctx.build_operator(cfg.Nx, cfg.Ny, cfg.Nz, cfg.edge, cfg.k, cfg.L, khat, T)
         ctx.sync()
         ops = []
-        for fmt, tol in cfg.formats:
+        fmts = cfg.formats
+        if args.formats:
+            want = {(f.split("@")[0], float(f.split("@")[1])) for f in args.formats.split(",")}
+            fmts = tuple(ft for ft in fmts if (ft[0], ft[1]) in want)
+        for fmt, tol in fmts:
             if fmt in ("tucker3d", "tt3d"):
                 op = ctx.compress(T[d0:d0 + dn].contiguous(), n, dn, fmt, tol)
             else:
@@ -242,6 +247,9 @@ def run_ours(args):
             t_step = float(tt[0])
             per_op = tt[1:].cpu().numpy()
 
+        if args.quick:   # profiling mode (ncu): the timed steps only
+            print(json.dumps({"quick": True, "ms_per_step": t_step, "launches": int(launches)}), flush=True)
+            return
         # DENSE (uncompressed) baseline for the overhead figure
         dense_ms = None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -313,8 +321,17 @@ def run_ours(args):
     if dname == "conv_z_dense":
         bound, unit, peak = "hbm", "GB/s", float(peaks["hbm_gbs"])
         achieved = kwork.get(dname, 0.0) / (dms * 1e-3) / 1e9
+    elif dname in kwork and args.gemm == "tc":
+        # tcgen05 kind::tf32 with the 3xTF32 split: 3 tensor MMAs per useful MAC, so the
+        # FP32-accurate tensor roofline is the TF32 dense peak / 3; TF32 = bf16 x 1/2 (guide's
+        # nominal ratio), bf16 = measured sustained (kernel timed inside a long step).
+        tf32 = 0.5 * float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+        bound, unit, peak = "tensor", "TFLOP/s", tf32 / 3.0
+        peak_src = f"{peak_src} bf16 sustained x 0.5 (TF32) / 3 (3xTF32 split) = {tf32 / 3:.1f}; raw TF32 {tf32:.1f}"
+        achieved = kwork[dname] / (dms * 1e-3) / 1e12
     elif dname in kwork:
         bound, unit, peak = "alu", "TFLOP/s", FFMA_PEAK_TFLOPS
+        peak_src = "derived FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)"
         achieved = kwork[dname] / (dms * 1e-3) / 1e12
     else:
         bound, unit, peak, achieved = "hbm", "GB/s", float(peaks["hbm_gbs"]), None
@@ -358,15 +375,16 @@ def run_ours(args):
         "data": "synthetic: eq.(7) operators built on GPU (FP64), GPU-compressed; CN(0,1) seeded signatures",
         "config": {"workload": f"config{args.config}: {cfg.Nx}x{cfg.Ny}x{cfg.Nz} boxes, padded {n[0]}x{n[1]}x{n[2]}, "
                                f"{ndir} dirs, edge {cfg.edge} lambda, L={cfg.L}; ops "
-                               + ",".join(f"{f}@{t:g}" for f, t in cfg.formats),
+                               + ",".join(f"{f}@{t:g}" for f, t, _ in ops),
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
-                   "parallelism": f"direction-shard x{world}"},
+                   "parallelism": f"direction-shard x{world}",
+                   "restore_gemm": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate" if args.gemm == "tc" else "FP32 FFMA"},
         "gpu_launches": int(launches),
         "roofline": {"bound": bound, "kernel": dname, "achieved": None if achieved is None else round(achieved, 3),
                      "peak": round(peak, 2), "unit": unit,
                      "frac": None if achieved is None else round(achieved / peak, 4),
                      "traffic": traffic,
-                     "peak_source": "derived FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if bound == "alu" else peak_src},
+                     "peak_source": peak_src},
         "e2e": {"value": round(e2e_value, 3), "unit": "Gdir*pt/s",
                 "h2d_bytes_per_step": int(len(ops) * (ndir * K * 8 + ndir * 4)),
                 "d2h_bytes_per_step": int(len(ops) * K * 8)},
@@ -492,6 +510,9 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="timed steps only (for ncu launch lists)")
+    ap.add_argument("--gemm", default="tc", choices=["tc", "ffma"], help="restore-GEMM kernel (A/B)")
+    ap.add_argument("--formats", default=None, help="comma list fmt@tol restricting the config's ops")
     ap.add_argument("--cpu-sample", type=int, default=24)
     ap.add_argument("--ref-sample", type=int, default=8)
     args = ap.parse_args()

@@ -101,6 +101,21 @@ fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_
 /* Number of kernels this context has launched since creation.               */
 int64_t fmmt_launch_count(const fmmt_ctx* ctx);
 
+/* Implementation of the restore GEMMs (Figs. 3-4 contractions): 1 = tcgen05
+ * tensor cores, kind::tf32 with the 3xTF32 split and FP32 accumulation
+ * (default); 0 = FP32 FFMA kernel (kept for A/B measurement).  Both are
+ * hand-written sm_100a kernels of this library; neither is a CPU path.       */
+fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl);
+
+/* Test hook (not the hot path): C = op(A) . op(B) for device complex64
+ * column-major matrices through the restore-GEMM kernel `impl` (as above).
+ * op(A) is m x k: transA = 0 reads A(i,l) at A[i + lda*l], 1 at A[l + lda*i].
+ * op(B) is k x n: transB = 0 reads B(l,j) at B[l + ldb*j], 1 at B[j + ldb*l].
+ * C(i,j) is written at C[i + ldc*j].  Asynchronous on the context stream.   */
+fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64_t k, int transA, int transB,
+                            const fmmt_c64* A, int64_t lda, const fmmt_c64* B, int64_t ldb,
+                            fmmt_c64* C, int64_t ldc);
+
 /* ------------------------------------------------------- setup: the operator */
 
 /* Multipole count L = floor(x + 1.8 digits^(2/3) x^(1/3)), x = 2|k|R^s,

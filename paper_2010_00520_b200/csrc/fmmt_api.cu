@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +25,7 @@
 #include "fmmt_internal.h"
 #include "kernels_fft.cuh"
 #include "kernels_gemm.cuh"
+#include "kernels_tcgemm.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -194,9 +196,11 @@ ZKernel get_z(int n3, int mode) {
 struct GemmLaunch {
   int first = 0;       // index into op->descs
   int ndesc = 0;
-  int maxtiles = 0;    // for the chosen tile size
+  int maxtiles = 0;    // FFMA kernel: for the chosen tile size
   int maxsub = 0;
-  bool big = false;    // 64x64 tiles
+  bool big = false;    // FFMA kernel: 64x64 tiles
+  int tc_bn = 64;      // tensor-core kernel: complex columns per tile
+  int tc_maxtiles = 0; // tensor-core kernel: tiles of 128 x tc_bn
   const char* name = "";
 };
 
@@ -217,6 +221,7 @@ struct fmmt_op {
   int64_t* d_voff = nullptr;                   // per direction offset of the z-stage V factor
   int* d_rank = nullptr;                       // per direction z-stage rank (3D formats)
   float2* tbar1 = nullptr;                     // TT-4D: T1 = U1 . C1 (Fig. 4(a) step 1), n1 n2 x r2
+  float2* E = nullptr;                         // H-Tucker: (C12 . C1234) x1 U1 x2 U2, n1 n2 x r34
   // workspace
   int64_t PB = 0;
   float2 *W = nullptr, *H = nullptr, *Gw = nullptr, *Cw = nullptr, *Mw = nullptr, *Nw = nullptr,
@@ -259,6 +264,7 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->d_voff) cudaFree(op->d_voff);
   if (op->d_rank) cudaFree(op->d_rank);
   if (op->tbar1) cudaFree(op->tbar1);
+  if (op->E) cudaFree(op->E);
   if (op->d_in_host) cudaFree(op->d_in_host);
   if (op->d_w_host) cudaFree(op->d_w_host);
   if (op->d_sum_host) cudaFree(op->d_sum_host);
@@ -273,10 +279,7 @@ static int64_t per_dir_ws(const fmmt_op* op) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D: e += op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
     case FMMT_TUCKER4D: e += rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) + op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
-    case FMMT_HTUCKER4D:
-      e += rk(op, 0, 2) * rk(op, 0, 5) + rk(op, 0, 4) * rk(op, 0, 2) + rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) +
-           op->n1 * op->r2max * op->r3max + n12 * op->r3max;
-      break;
+    case FMMT_HTUCKER4D: e += rk(op, 0, 2) * rk(op, 0, 5) + n12 * op->r3max; break;
     case FMMT_TT3D: e += n12 * op->rGmax; break;
     case FMMT_TT4D: e += rk(op, 0, 1) * op->n3; break;
   }
@@ -304,29 +307,78 @@ static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, con
   }
   L.big = (mmin >= 64 && nmin >= 64);
   const int bm = L.big ? 64 : 32, bn = L.big ? 64 : 32;
+  L.tc_bn = nmin >= 64 ? 64 : (nmin >= 32 ? 32 : 16);
   for (auto& d : ds) {
     int tiles = ((d.m + bm - 1) / bm) * ((d.n + bn - 1) / bn);
     L.maxtiles = std::max(L.maxtiles, tiles);
+    L.tc_maxtiles = std::max(L.tc_maxtiles, ((d.m + fmmt::TC_BM - 1) / fmmt::TC_BM) * ((d.n + L.tc_bn - 1) / L.tc_bn));
     L.maxsub = std::max(L.maxsub, d.batch);
     op->descs.push_back(d);
   }
   b.gemms.push_back(L);
 }
 
+// Column-major helper: C (ldc) = A (m x k, lda) . op(B), op(B) = B (k x n, ldb) or
+// B^T when B is stored n x k (transB).  Sub-batch strides sA, sB, sC.
 static GemmDesc gd(const float2* A, const float2* B, float2* C, int64_t m, int64_t n, int64_t k, int transB,
                    int64_t lda, int64_t ldb, int64_t ldc, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
   GemmDesc d;
+  memset(&d, 0, sizeof(d));
   d.A = A; d.B = B; d.C = C;
   d.m = (int)m; d.n = (int)n; d.k = (int)k;
-  d.transB = transB; d.batch = batch;
-  d.lda = lda; d.ldb = ldb; d.ldc = ldc;
+  d.batch = batch;
+  d.a_s0 = 1; d.a_s1 = 0; d.a_div = 1 << 30; d.a_sk = lda;
+  if (transB) { d.b_sk = ldb; d.b_sn = 1; } else { d.b_sk = 1; d.b_sn = ldb; }
+  d.c_s0 = 1; d.c_s1 = 0; d.c_div = 1 << 30; d.c_sn = ldc;
   d.sA = sA; d.sB = sB; d.sC = sC;
   return d;
+}
+
+// General helper: A(i,l) = A[(i%a_div)*a_s0 + (i/a_div)*a_s1 + l*a_sk], B(l,j) = B[l*b_sk + j*b_sn],
+// C(i,j) = C[(i%c_div)*c_s0 + (i/c_div)*c_s1 + j*c_sn].
+static GemmDesc gdx(const float2* A, const float2* B, float2* C, int64_t m, int64_t n, int64_t k, int64_t a_s0,
+                    int64_t a_s1, int64_t a_div, int64_t a_sk, int64_t b_sk, int64_t b_sn, int64_t c_s0, int64_t c_s1,
+                    int64_t c_div, int64_t c_sn, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+  GemmDesc d;
+  memset(&d, 0, sizeof(d));
+  d.A = A; d.B = B; d.C = C;
+  d.m = (int)m; d.n = (int)n; d.k = (int)k;
+  d.batch = batch;
+  d.a_s0 = a_s0; d.a_s1 = a_s1; d.a_div = (int)std::min<int64_t>(a_div, 1 << 30); d.a_sk = a_sk;
+  d.b_sk = b_sk; d.b_sn = b_sn;
+  d.c_s0 = c_s0; d.c_s1 = c_s1; d.c_div = (int)std::min<int64_t>(c_div, 1 << 30); d.c_sn = c_sn;
+  d.sA = sA; d.sB = sB; d.sC = sC;
+  return d;
+}
+constexpr int64_t NODIV = 1 << 30;
+
+static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d_descs, int impl);
+
+// One GEMM outside any plan (setup-time derived factors, the test hook).  Asynchronous.
+static fmmt_status run_one_gemm(fmmt_ctx* ctx, const GemmDesc& d, int impl, const char* name) {
+  fmmt_op tmp;
+  tmp.ctx = ctx;
+  Batch b;
+  add_gemm(&tmp, b, {d}, name);
+  GemmDesc* dd = nullptr;
+  FMMT_CUDA(ctx, cudaMallocAsync((void**)&dd, sizeof(GemmDesc), ctx->stream));
+  FMMT_CUDA(ctx, cudaMemcpyAsync(dd, &d, sizeof(GemmDesc), cudaMemcpyHostToDevice, ctx->stream));
+  fmmt_status st;
+  {
+    ProfScope ps(ctx, name);
+    st = launch_gemm_group(ctx, b.gemms[0], dd, impl);
+  }
+  cudaFreeAsync(dd, ctx->stream);
+  return st;
 }
 
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
 static void tucker_chain(fmmt_op* op, Batch& b) {
+  // Fig. 3(a) in the "tall" orientation so every GEMM has >= n1*r rows:
+  //   mode 1:  H_q[(b + r2 c) + r2 r3 i] = sum_a core_q[a + r1 (b + r2 c)] U1[i + n1 a]
+  //   mode 2:  G_q[i + n1 j + n12 c]     = sum_b H_q[b + r2 c + r2 r3 i] U2[j + n2 b]
+  // G_q is [c][ij], the layout the fused z-stage reads (A(ij, c), K = r3).
   const int64_t n1 = op->n1, n2 = op->n2, n12 = n1 * n2;
   std::vector<GemmDesc> sa, sb;
   if (op->format == FMMT_TUCKER3D) {
@@ -338,15 +390,17 @@ static void tucker_chain(fmmt_op* op, Batch& b) {
       const float2* U2 = op->arr[2] + op->off[2][p];
       float2* Hq = op->H + q * n1 * op->r2max * op->r3max;
       float2* Gq = op->Gw + q * n12 * op->rGmax;
-      sa.push_back(gd(U1, core, Hq, n1, r2 * r3, r1, 0, n1, r1, n1));
-      sb.push_back(gd(Hq, U2, Gq, n1, n2, r2, 1, n1, n2, n1, (int)r3, n1 * r2, 0, n12));
+      sa.push_back(gdx(core, U1, Hq, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3));
+      sb.push_back(gdx(Hq, U2, Gq, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1));
     }
   } else {
     const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
     const float2* U1 = op->arr[op->format == FMMT_TUCKER4D ? 1 : 0];
     const float2* U2 = op->arr[op->format == FMMT_TUCKER4D ? 2 : 1];
-    sa.push_back(gd(U1, op->Cw, op->H, n1, r2 * r3, r1, 0, n1, r1, n1, b.nq, 0, r1 * r2 * r3, n1 * r2 * r3));
-    sb.push_back(gd(op->H, U2, op->Gw, n1, n2, r2, 1, n1, n2, n1, (int)(b.nq * r3), n1 * r2, 0, n12));
+    sa.push_back(gdx(op->Cw, U1, op->H, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3, b.nq,
+                     r1 * r2 * r3, 0, n1 * r2 * r3));
+    sb.push_back(gdx(op->H, U2, op->Gw, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1, b.nq,
+                     n1 * r2 * r3, 0, n12 * r3));
   }
   add_gemm(op, b, sa, "restore_mode1");
   add_gemm(op, b, sb, "restore_mode2");
@@ -380,9 +434,6 @@ static fmmt_status build_plans(fmmt_op* op) {
       break;
     case FMMT_HTUCKER4D:
       if ((st = cmalloc(op, &op->Mw, PB * rk(op, 0, 2) * rk(op, 0, 5)))) return st;
-      if ((st = cmalloc(op, &op->Nw, PB * rk(op, 0, 4) * rk(op, 0, 2)))) return st;
-      if ((st = cmalloc(op, &op->Cw, PB * rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2)))) return st;
-      if ((st = cmalloc(op, &op->H, PB * n1 * op->r2max * op->r3max))) return st;
       if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
       break;
     case FMMT_TT3D:
@@ -408,28 +459,28 @@ static fmmt_status build_plans(fmmt_op* op) {
         break;
       }
       case FMMT_HTUCKER4D: {
-        const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3), r12 = rk(op, 0, 4),
-                      r34 = rk(op, 0, 5);
-        const float2 *U4 = op->arr[3], *C12 = op->arr[4], *C34 = op->arr[5], *C1234 = op->arr[6];
-        // a3 (Fig. 3(c)): M_q[c,j] = sum_d C34[c,d,j] U4[p,d]
-        add_gemm(op, b, {gd(C34, U4 + b.q0, op->Mw, r3, b.nq, r4, 1, r3, op->ndir, r3 * r34, (int)r34, r3 * r4, 0, r3)},
+        // Fig. 3(c) with the direction-independent part precomputed once per op
+        // (E = (C12 . C1234) x1 U1 x2 U2, n1 n2 x r34; create_op):
+        //   M_q[c, j] = sum_d C34[c + r3 d + r3 r4 j] U4[p, d]      (a3)  stored Mw[c + r3 q + r3 nq j]
+        //   G_q[ij, c] = sum_j E[ij + n12 j] M_q[c, j]              (a4)  stored Gw[ij + n12 (c + r3 q)]
+        const int64_t r3 = rk(op, 0, 2), r4 = rk(op, 0, 3), r34 = rk(op, 0, 5);
+        const int64_t nq = b.nq;
+        const float2 *U4 = op->arr[3], *C34 = op->arr[5];
+        add_gemm(op, b, {gdx(C34, U4 + b.q0, op->Mw, r3 * r34, nq, r4, 1, r3 * r4, r3, r3, op->ndir, 1, 1, r3 * nq, r3, r3)},
                  "slice_htucker_M");
-        // N_q = C1234 . M_q^T  (r12 x r3)
-        add_gemm(op, b, {gd(C1234, op->Mw, op->Nw, r12, r3, r34, 1, r12, r3, r12, b.nq, 0, r3 * r34, r12 * r3)},
-                 "slice_htucker_N");
-        // C_q = C12(r1 r2 x r12) . N_q  (r1 r2 x r3)
-        add_gemm(op, b, {gd(C12, op->Nw, op->Cw, r1 * r2, r3, r12, 0, r1 * r2, r12, r1 * r2, b.nq, 0, r12 * r3, r1 * r2 * r3)},
-                 "slice_htucker_C");
-        tucker_chain(op, b);
+        add_gemm(op, b, {gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12)},
+                 "slice_htucker_G");
         break;
       }
       case FMMT_TT3D: {
         std::vector<GemmDesc> ds;
+        // Fig. 4(a): G_q[i + n1 j + n12 b] = sum_a C1_q[a + r1 (j + n2 b)] U1_q[i + n1 a]
+        // (rows (j, b), n2 r2 of them; G_q is [b][ij] for the z-stage)
         for (int q = 0; q < b.nq; ++q) {
           const int64_t p = b.q0 + q;
           const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1);
-          ds.push_back(gd(op->arr[0] + op->off[0][p], op->arr[1] + op->off[1][p], op->Gw + q * n12 * op->rGmax, n1,
-                          n2 * r2, r1, 0, n1, r1, n1));
+          ds.push_back(gdx(op->arr[1] + op->off[1][p], op->arr[0] + op->off[0][p], op->Gw + q * n12 * op->rGmax,
+                           n2 * r2, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, n12, n2, 1));
         }
         add_gemm(op, b, ds, "restore_tt_head");
         break;
@@ -452,17 +503,39 @@ static fmmt_status build_plans(fmmt_op* op) {
 }
 
 // ============================================================== launches
+template <int BN>
+static fmmt_status launch_tc_bn(fmmt_ctx* ctx, dim3 grid, const GemmDesc* d) {
+  using Cfg = fmmt::TcGemmCfg<BN>;
+  FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)fmmt::k_tc_cgemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  fmmt::k_tc_cgemm<BN><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
+  return FMMT_OK;
+}
+
+// Launch one descriptor group.  impl: 0 = FP32 FFMA kernel, 1 = tcgen05 3xTF32.
+static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d_descs, int impl) {
+  if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
+  fmmt_status st = FMMT_OK;
+  if (impl == 1) {
+    dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
+    if (L.tc_bn == 64) st = launch_tc_bn<64>(ctx, grid, d_descs + L.first);
+    else if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, grid, d_descs + L.first);
+    else st = launch_tc_bn<16>(ctx, grid, d_descs + L.first);
+  } else {
+    dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
+    if (L.big)
+      fmmt::k_cgemm<64, 64, 16, 4, 4><<<grid, 256, 0, ctx->stream>>>(d_descs + L.first);
+    else
+      fmmt::k_cgemm<32, 32, 16, 4, 4><<<grid, 64, 0, ctx->stream>>>(d_descs + L.first);
+  }
+  if (st) return st;
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
 static fmmt_status launch_gemm(fmmt_op* op, const GemmLaunch& L) {
   fmmt_ctx* ctx = op->ctx;
   ProfScope ps(ctx, L.name);
-  dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
-  if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
-  if (L.big)
-    fmmt::k_cgemm<64, 64, 16, 4, 4><<<grid, 256, 0, ctx->stream>>>(op->d_descs + L.first);
-  else
-    fmmt::k_cgemm<32, 32, 16, 4, 4><<<grid, 64, 0, ctx->stream>>>(op->d_descs + L.first);
-  FMMT_CUDA(ctx, cudaGetLastError());
-  return FMMT_OK;
+  return launch_gemm_group(ctx, L, op->d_descs, ctx->gemm_impl);
 }
 
 static int xy_ppc(const XYKernels& k) {
@@ -521,8 +594,37 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
   }
 }
 
+template <int N3>
+static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, dim3 grid, const ZArgs& a) {
+  using Cfg = fmmt::TcGemmCfg<(N3 < 16 ? 16 : N3)>;
+  const void* fn = mode == fmmt::Z_RESTORE ? (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE>
+                                           : (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK>;
+  FMMT_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  if (mode == fmmt::Z_RESTORE) fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
+  else fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout) {
   fmmt_ctx* ctx = op->ctx;
+  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
+    ZArgs a;
+    fill_zargs(op, a);
+    a.W = op->W + (int64_t)qoff * (op->n3 / 2) * a.n12;
+    a.p0 = p0;
+    a.G = a.G + (int64_t)qoff * a.g_stride;
+    if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
+    a.Tout = Tout;
+    dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)nq);
+    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : "restore_conv_z");
+    switch (op->n3) {
+      case 4: return launch_tc_z<4>(ctx, mode, grid, a);
+      case 8: return launch_tc_z<8>(ctx, mode, grid, a);
+      case 16: return launch_tc_z<16>(ctx, mode, grid, a);
+      default: return launch_tc_z<32>(ctx, mode, grid, a);
+    }
+  }
   ZKernel k = get_z((int)op->n3, mode);
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
   ZArgs a;
@@ -624,6 +726,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   ctx->stream = (cudaStream_t)cuda_stream;
   ctx->rank = rank;
   ctx->world = world;
+  if (const char* e = getenv("FMMT_GEMM")) ctx->gemm_impl = (strcmp(e, "ffma") == 0) ? 0 : 1;
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, 128);
@@ -699,6 +802,25 @@ fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_
 
 int64_t fmmt_launch_count(const fmmt_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl) {
+  if (!ctx || (impl != 0 && impl != 1)) return FMMT_E_ARG;
+  ctx->gemm_impl = impl;
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64_t k, int transA, int transB,
+                            const fmmt_c64* A, int64_t lda, const fmmt_c64* B, int64_t ldb, fmmt_c64* C, int64_t ldc) {
+  if (!ctx) return FMMT_E_ARG;
+  CHECK_ARG(ctx, impl == 0 || impl == 1, "impl must be 0 or 1");
+  CHECK_ARG(ctx, A && B && C, "null matrix");
+  CHECK_SHAPE(ctx, m >= 1 && n >= 1 && k >= 1 && m < (1 << 30) && n < (1 << 30) && k < (1 << 30), "bad gemm dims");
+  cudaSetDevice(ctx->device);
+  GemmDesc d = gd(reinterpret_cast<const float2*>(A), reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(C),
+                  m, n, k, transB, lda, ldb, ldc);
+  if (transA) { d.a_s0 = lda; d.a_sk = 1; }
+  return run_one_gemm(ctx, d, impl, "test_cgemm");
+}
+
 fmmt_status fmmt_op_import(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
                            const int64_t* ranks, const fmmt_c64* const* arrays, int64_t narrays, fmmt_op** op) {
   return fmmt_internal::create_op(ctx, format, n1, n2, n3, ndir, ranks, (const void* const*)arrays, narrays, op);
@@ -727,7 +849,8 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
   for (auto e : op->arr_elems) comp += e;
   info->compressed_bytes = comp * 8;
   info->original_bytes = op->n1 * op->n2 * op->n3 * op->ndir * 8;
-  info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0);
+  info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0) +
+                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0);
   info->batch = op->PB;
   // restore complex MACs per matvec (a3 + a4), in the contraction order the kernels use
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n = n1 * n2 * n3;
@@ -735,14 +858,16 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
   for (int64_t p = 0; p < op->ndir; ++p) {
     switch (op->format) {
       case FMMT_DENSE: break;
-      case FMMT_TUCKER3D: case FMMT_TUCKER4D: case FMMT_HTUCKER4D: {
+      case FMMT_TUCKER3D: case FMMT_TUCKER4D: {
         const double r1 = rk(op, p, 0), r2 = rk(op, p, 1), r3 = rk(op, p, 2);
         cm += n1 * r1 * r2 * r3 + n1 * n2 * r2 * r3 + (double)n * r3;
         if (op->format == FMMT_TUCKER4D) cm += r1 * r2 * r3 * rk(op, 0, 3);
-        if (op->format == FMMT_HTUCKER4D) {
-          const double r4 = rk(op, 0, 3), r12 = rk(op, 0, 4), r34 = rk(op, 0, 5);
-          cm += r3 * r4 * r34 + r12 * r34 * r3 + r1 * r2 * r12 * r3;
-        }
+        break;
+      }
+      case FMMT_HTUCKER4D: {
+        // M_p (r3 r4 r34) + G_p = E . M_p^T (n1 n2 r34 r3) + z-stage (n r3); E is per op
+        const double r3 = rk(op, 0, 2), r4 = rk(op, 0, 3), r34 = rk(op, 0, 5);
+        cm += r3 * r4 * r34 + (double)n1 * n2 * r34 * r3 + (double)n * r3;
         break;
       }
       case FMMT_TT3D: {
@@ -995,6 +1120,34 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     cudaMalloc(&op->d_rank, ndir * sizeof(int));
     cudaMemcpy(op->d_voff, voff.data(), ndir * sizeof(int64_t), cudaMemcpyHostToDevice);
     cudaMemcpy(op->d_rank, rz.data(), ndir * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  if (format == FMMT_HTUCKER4D) {
+    // Direction-independent part of Fig. 3(c), once per op:
+    //   D  = C12 (r1 r2 x r12) . C1234 (r12 x r34)
+    //   E1[i + n1 b + n1 r2 j] = sum_a D[a + r1 (b + r2 j)] U1[i + n1 a]
+    //   E [i + n1 jj + n12 j]  = sum_b E1[i + n1 b + n1 r2 j] U2[jj + n2 b]
+    const int64_t r1 = R(0, 0), r2 = R(0, 1), r12 = R(0, 4), r34 = R(0, 5), n12 = n1 * n2;
+    float2 *D = nullptr, *E1 = nullptr;
+    if (cudaMalloc(&op->E, n12 * r34 * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&D, r1 * r2 * r34 * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&E1, n1 * r2 * r34 * sizeof(float2)) != cudaSuccess) {
+      if (D) cudaFree(D);
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_NOMEM, "H-Tucker E allocation failed");
+    }
+    fmmt_status st = run_one_gemm(ctx, gd(op->arr[4], op->arr[6], D, r1 * r2, r34, r12, 0, r1 * r2, r12, r1 * r2), ctx->gemm_impl,
+                                  "htucker_D");
+    if (!st) st = run_one_gemm(ctx, gdx(D, op->arr[0], E1, r2 * r34, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, 0, NODIV, 1),
+                               ctx->gemm_impl, "htucker_E1");
+    if (!st) st = run_one_gemm(ctx, gdx(E1, op->arr[1], op->E, n1 * r34, n2, r2, 1, n1 * r2, n1, n1, n2, 1, 1, n12, n1, n1),
+                               ctx->gemm_impl, "htucker_E");
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(D);
+    cudaFree(E1);
+    if (st || e != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return st ? st : set_err(ctx, FMMT_E_CUDA, "H-Tucker E gemm failed: %s", cudaGetErrorString(e));
+    }
   }
   fmmt_status st = build_plans(op);
   if (st) {

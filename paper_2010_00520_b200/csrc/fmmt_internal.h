@@ -24,6 +24,7 @@ struct fmmt_ctx {
   std::string err;
   int64_t launches = 0;
   bool profiling = false;
+  int gemm_impl = 1;                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
   std::vector<fmmt_prof_entry> pending;
   std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
   std::vector<cudaEvent_t> event_pool;

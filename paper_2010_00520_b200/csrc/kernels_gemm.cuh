@@ -5,7 +5,7 @@
 //   H-Tucker (Fig. 3(c)):       M_p, N_p = C1234 . M_p^T, C_p = C12 . N_p (a3)
 //   TT-3D (Fig. 4(a)):   G_p = U1_p . C1_p
 //   TT-4D (Fig. 4(b)):   T2 columns  V_p = C2 . U_last[p,:]^T      (a3)
-// Every call is C = A . op(B) with column-major operands; a descriptor list
+// Every call is C = A . B with general (two-level) strides; a descriptor list
 // gives one (possibly strided-batched) GEMM per entry so that directions
 // with different ranks (3D formats) run in one launch.
 #pragma once
@@ -18,11 +18,24 @@ struct GemmDesc {
   const float2* B;
   float2* C;
   int m, n, k;
-  int transB;          // 0: B is k x n (ldb); 1: B is stored n x k (ldb), op(B) = B^T
   int batch;           // strided sub-batch count
-  int64_t lda, ldb, ldc;
+  // A(i,l) = A[(i % a_div) * a_s0 + (i / a_div) * a_s1 + l * a_sk]   (two-level row index)
+  int64_t a_s0, a_s1, a_sk;
+  int a_div;
+  // B(l,j) = B[l * b_sk + j * b_sn]
+  int64_t b_sk, b_sn;
+  // C(i,j) = C[(i % c_div) * c_s0 + (i / c_div) * c_s1 + j * c_sn]
+  int64_t c_s0, c_s1, c_sn;
+  int c_div;
   int64_t sA, sB, sC;  // sub-batch strides (elements)
 };
+
+__device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {
+  return (int64_t)(i % d.a_div) * d.a_s0 + (int64_t)(i / d.a_div) * d.a_s1;
+}
+__device__ __forceinline__ int64_t c_row(const GemmDesc& d, int i) {
+  return (int64_t)(i % d.c_div) * d.c_s0 + (int64_t)(i / d.c_div) * d.c_s1;
+}
 
 template <int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
@@ -58,19 +71,19 @@ k_cgemm(const GemmDesc* __restrict__ descs) {
     for (int e = tid; e < BM * BK; e += NT) {
       const int i = e % BM, kk = e / BM;
       const int gm = m0 + i, gk = k0 + kk;
-      As[kk][i] = (gm < d.m && gk < d.k) ? A[gm + d.lda * gk] : make_float2(0.f, 0.f);
+      As[kk][i] = (gm < d.m && gk < d.k) ? A[a_row(d, gm) + gk * d.a_sk] : make_float2(0.f, 0.f);
     }
-    if (d.transB) {
+    if (d.b_sk != 1) {
       for (int e = tid; e < BN * BK; e += NT) {
         const int j = e % BN, kk = e / BN;
         const int gn = n0 + j, gk = k0 + kk;
-        Bs[kk][j] = (gn < d.n && gk < d.k) ? B[gn + d.ldb * gk] : make_float2(0.f, 0.f);
+        Bs[kk][j] = (gn < d.n && gk < d.k) ? B[gn * d.b_sn + gk * d.b_sk] : make_float2(0.f, 0.f);
       }
     } else {
       for (int e = tid; e < BN * BK; e += NT) {
         const int kk = e % BK, j = e / BK;
         const int gn = n0 + j, gk = k0 + kk;
-        Bs[kk][j] = (gn < d.n && gk < d.k) ? B[gk + d.ldb * gn] : make_float2(0.f, 0.f);
+        Bs[kk][j] = (gn < d.n && gk < d.k) ? B[gk + d.b_sn * gn] : make_float2(0.f, 0.f);
       }
     }
     __syncthreads();
@@ -100,10 +113,11 @@ k_cgemm(const GemmDesc* __restrict__ descs) {
   for (int i = 0; i < TM; ++i) {
     const int gm = m0 + ty * TM + i;
     if (gm >= d.m) continue;
+    const int64_t cr = c_row(d, gm);
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int gn = n0 + tx * TN + j;
-      if (gn < d.n) C[gm + d.ldc * gn] = acc[i][j];
+      if (gn < d.n) C[cr + d.c_sn * gn] = acc[i][j];
     }
   }
 }

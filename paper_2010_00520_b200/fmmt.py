@@ -76,13 +76,15 @@ fmmt_translate = _sig("fmmt_translate", C.c_int, vp, vp, vp, i64, i64, i64, i64)
 fmmt_translate_sum = _sig("fmmt_translate_sum", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64)
 fmmt_translate_sum_host = _sig("fmmt_translate_sum_host", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64)
 fmmt_restore = _sig("fmmt_restore", C.c_int, vp, i64, vp)
+fmmt_set_gemm_impl = _sig("fmmt_set_gemm_impl", C.c_int, vp, C.c_int)
+fmmt_test_cgemm = _sig("fmmt_test_cgemm", C.c_int, vp, C.c_int, i64, i64, i64, C.c_int, C.c_int, vp, i64, vp, i64, vp, i64)
 
 EXPORTED = [
     "fmmt_version", "fmmt_init", "fmmt_init_sharded", "fmmt_nccl_unique_id", "fmmt_destroy", "fmmt_sync",
     "fmmt_last_error", "fmmt_shard_range", "fmmt_set_profiling", "fmmt_prof_reset", "fmmt_prof_read",
     "fmmt_launch_count", "fmmt_multipole_count", "fmmt_direction_grid", "fmmt_build_operator", "fmmt_compress",
     "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_set_batch", "fmmt_translate",
-    "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore",
+    "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
 ]
 
 
@@ -182,6 +184,13 @@ class Context:
         la = (C.c_int64 * 64)()
         _check(fmmt_prof_read(self.h, names, ms, la, 64, C.byref(cnt)), self.h, "fmmt_prof_read")
         return {names[i].decode(): (ms[i], la[i]) for i in range(min(64, cnt.value))}
+
+    def set_gemm_impl(self, impl: str):
+        _check(fmmt_set_gemm_impl(self.h, {"ffma": 0, "tc": 1}[impl]), self.h, "fmmt_set_gemm_impl")
+
+    def test_cgemm(self, impl: str, m, n, k, A, lda, B, ldb, Cout, ldc, transA=0, transB=0):
+        _check(fmmt_test_cgemm(self.h, {"ffma": 0, "tc": 1}[impl], m, n, k, transA, transB, _ptr(A), lda, _ptr(B), ldb,
+                               _ptr(Cout), ldc), self.h, "fmmt_test_cgemm")
 
     def build_operator(self, Nx, Ny, Nz, edge, k, L, khat: np.ndarray, out):
         khat = np.ascontiguousarray(khat, dtype=np.float64)
