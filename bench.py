@@ -144,6 +144,13 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def workload_str(cfg_index, formats):
+    cfg = get_config(cfg_index)
+    n = cfg.n
+    return (f"config{cfg_index}: {cfg.Nx}x{cfg.Ny}x{cfg.Nz} boxes, padded {n[0]}x{n[1]}x{n[2]}, "
+            f"{cfg.ndir} dirs, edge {cfg.edge} lambda, L={cfg.L}; ops " + ",".join(f"{f}@{t:g}" for f, t in formats))
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -321,7 +328,7 @@ def run_ours(args):
     if dname == "conv_z_dense":
         bound, unit, peak = "hbm", "GB/s", float(peaks["hbm_gbs"])
         achieved = kwork.get(dname, 0.0) / (dms * 1e-3) / 1e9
-    elif dname in kwork and args.gemm == "tc":
+    elif dname in kwork and args.gemm in ("tc", "tc1"):
         # tcgen05 kind::tf32 with the 3xTF32 split: 3 tensor MMAs per useful MAC, so the
         # FP32-accurate tensor roofline is the TF32 dense peak / 3; TF32 = bf16 x 1/2 (guide's
         # nominal ratio), bf16 = measured sustained (kernel timed inside a long step).
@@ -373,12 +380,10 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "c64",
         "data": "synthetic: eq.(7) operators built on GPU (FP64), GPU-compressed; CN(0,1) seeded signatures",
-        "config": {"workload": f"config{args.config}: {cfg.Nx}x{cfg.Ny}x{cfg.Nz} boxes, padded {n[0]}x{n[1]}x{n[2]}, "
-                               f"{ndir} dirs, edge {cfg.edge} lambda, L={cfg.L}; ops "
-                               + ",".join(f"{f}@{t:g}" for f, t, _ in ops),
+        "config": {"workload": workload_str(args.config, [(f, t) for f, t, _ in ops]),
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": f"direction-shard x{world}",
-                   "restore_gemm": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate" if args.gemm == "tc" else "FP32 FFMA"},
+                   "restore_gemm": {"tc": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate (persistent, warp-specialised)", "tc1": "tcgen05 kind::tf32, 3xTF32 (first design)", "ffma": "FP32 FFMA"}[args.gemm]},
         "gpu_launches": int(launches),
         "roofline": {"bound": bound, "kernel": dname, "achieved": None if achieved is None else round(achieved, 3),
                      "peak": round(peak, 2), "unit": unit,
@@ -493,7 +498,8 @@ def run_reference(args):
         "value": round(v, 6), "unit": "Gdir*pt/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic (oracle-built operators)",
-        "config": {"workload": f"config{args.config} (oracle sample)", "parallelism": "host cores"},
+        "config": {"workload": workload_str(args.config, list(c.formats)), "parallelism": "host cores",
+                   "sample": f"{len(sample)} of {c.ndir} directions per op"},
         "cpu_baseline": {"value": round(v, 6), "unit": "Gdir*pt/s", "cores": os.cpu_count(), "kind": "oracle",
                          "sample": f"{len(sample)} of {c.ndir} directions per op, ops "
                                    + ",".join(f"{f}@{t:g}" for f, t, _ in ops) + f"; setup {setup:.0f}s untimed"},
@@ -511,7 +517,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed steps only (for ncu launch lists)")
-    ap.add_argument("--gemm", default="tc", choices=["tc", "ffma"], help="restore-GEMM kernel (A/B)")
+    ap.add_argument("--gemm", default="tc", choices=["tc", "tc1", "ffma"], help="restore-GEMM kernel (A/B)")
     ap.add_argument("--formats", default=None, help="comma list fmt@tol restricting the config's ops")
     ap.add_argument("--cpu-sample", type=int, default=24)
     ap.add_argument("--ref-sample", type=int, default=8)

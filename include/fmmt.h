@@ -102,9 +102,11 @@ fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_
 int64_t fmmt_launch_count(const fmmt_ctx* ctx);
 
 /* Implementation of the restore GEMMs (Figs. 3-4 contractions): 1 = tcgen05
- * tensor cores, kind::tf32 with the 3xTF32 split and FP32 accumulation
- * (default); 0 = FP32 FFMA kernel (kept for A/B measurement).  Both are
- * hand-written sm_100a kernels of this library; neither is a CPU path.       */
+ * tensor cores, kind::tf32 with the 3xTF32 split and FP32 accumulation,
+ * persistent warp-specialised kernels (default); 2 = the first tcgen05 design
+ * (non-persistent); 0 = FP32 FFMA kernel.  2 and 0 are kept for A/B
+ * measurement.  All are hand-written sm_100a kernels of this library; none is
+ * a CPU path.                                                                */
 fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl);
 
 /* Test hook (not the hot path): C = op(A) . op(B) for device complex64
@@ -199,6 +201,13 @@ fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_
 fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs_per_batch);
 
 /* ------------------------------------------------------------ the hot path */
+
+/* Execution: the launches of one matvec (translate or translate_sum) are
+ * replayed as a CUDA graph: the first call with a given set of buffers runs
+ * directly, the second captures, later calls replay (one cudaGraphLaunch).
+ * Not used on the legacy default stream, while profiling, or with the
+ * environment variable FMMT_GRAPHS=0.  Call fmmt_set_gemm_impl before the
+ * first translate of an op.                                                  */
 
 /* Translation, eq. (5), for the op's ndir directions:
  *   sig_out[p] = truncate_{Nx,Ny,Nz}( F^{-1}( T_p (.) F( pad(sig_in[p]) ) ) )

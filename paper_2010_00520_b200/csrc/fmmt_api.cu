@@ -20,12 +20,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "fmmt_internal.h"
 #include "kernels_fft.cuh"
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
+#include "kernels_tcgemm_v1.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -77,13 +80,13 @@ struct ProfScope {
     ctx->launches++;
     if (ctx->profiling) {
       e0 = take_event(ctx);
-      cudaEventRecord(e0, ctx->stream);
+      cudaEventRecordWithFlags(e0, ctx->stream, cudaEventRecordExternal);   // graph node when captured
     }
   }
   ~ProfScope() {
     if (ctx->profiling) {
       cudaEvent_t e1 = take_event(ctx);
-      cudaEventRecord(e1, ctx->stream);
+      cudaEventRecordWithFlags(e1, ctx->stream, cudaEventRecordExternal);
       ctx->pending.push_back({name, e0, e1});
     }
   }
@@ -92,6 +95,8 @@ struct ProfScope {
 static void prof_flush(fmmt_ctx* ctx) {
   if (ctx->pending.empty()) return;
   cudaStreamSynchronize(ctx->stream);
+  for (auto ex : ctx->prof_execs) cudaGraphExecDestroy((cudaGraphExec_t)ex);
+  ctx->prof_execs.clear();
   for (auto& pe : ctx->pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, pe.e0, pe.e1);
@@ -111,6 +116,19 @@ static void prof_flush(fmmt_ctx* ctx) {
 }
 
 // ============================================================== kernel dispatch
+// Raise a kernel's dynamic shared-memory limit once per process (not per launch:
+// the call is host-side work on the launch path and must stay out of graph capture).
+static cudaError_t set_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[fn] = bytes;
+  return e;
+}
+
 namespace {
 
 struct XYKernels {
@@ -232,6 +250,14 @@ struct fmmt_op {
   GemmDesc* d_descs = nullptr;
   std::vector<Batch> batches;
   int nsplit = 1;
+  // CUDA graphs of whole matvecs, keyed by the buffers they read / write
+  struct GraphEntry {
+    const void* key[4];
+    int calls = 0;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;   // kernels inside the graph
+  };
+  std::vector<GraphEntry> graphs;
   // host staging for translate_sum_host
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
@@ -265,6 +291,8 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->d_rank) cudaFree(op->d_rank);
   if (op->tbar1) cudaFree(op->tbar1);
   if (op->E) cudaFree(op->E);
+  for (auto& g : op->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (op->d_in_host) cudaFree(op->d_in_host);
   if (op->d_w_host) cudaFree(op->d_w_host);
   if (op->d_sum_host) cudaFree(op->d_sum_host);
@@ -504,22 +532,40 @@ static fmmt_status build_plans(fmmt_op* op) {
 
 // ============================================================== launches
 template <int BN>
-static fmmt_status launch_tc_bn(fmmt_ctx* ctx, dim3 grid, const GemmDesc* d) {
+static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
   using Cfg = fmmt::TcGemmCfg<BN>;
-  FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)fmmt::k_tc_cgemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  fmmt::k_tc_cgemm<BN><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
+  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN>, Cfg::SMEM));
+  const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // persistent
+  fmmt::k_tc_cgemm<BN><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, L.ndesc);
   return FMMT_OK;
 }
 
-// Launch one descriptor group.  impl: 0 = FP32 FFMA kernel, 1 = tcgen05 3xTF32.
+template <int BN, int SPLIT = 0>
+static fmmt_status launch_tc1_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
+  using Cfg = fmmt::v1::TcGemmCfg<BN>;
+  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::v1::k_tc_cgemm<BN, SPLIT>, Cfg::SMEM));
+  dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
+  fmmt::v1::k_tc_cgemm<BN, SPLIT><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
+  return FMMT_OK;
+}
+
+// Launch one descriptor group.  impl: 0 = FP32 FFMA kernel, 1 = tcgen05 3xTF32
+// (persistent, warp-specialised), 2 = tcgen05 3xTF32 first design (A/B).
 static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d_descs, int impl) {
   if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
   fmmt_status st = FMMT_OK;
-  if (impl == 1) {
-    dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
-    if (L.tc_bn == 64) st = launch_tc_bn<64>(ctx, grid, d_descs + L.first);
-    else if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, grid, d_descs + L.first);
-    else st = launch_tc_bn<16>(ctx, grid, d_descs + L.first);
+  if (impl == 3 || impl == 4) {   // split experiments (test hook only)
+    if (impl == 3) st = launch_tc1_bn<64, 1>(ctx, L, d_descs + L.first);
+    else st = launch_tc1_bn<64, 2>(ctx, L, d_descs + L.first);
+  } else if (impl == 2) {
+    if (L.tc_bn == 64) st = launch_tc1_bn<64>(ctx, L, d_descs + L.first);
+    else if (L.tc_bn == 32) st = launch_tc1_bn<32>(ctx, L, d_descs + L.first);
+    else st = launch_tc1_bn<16>(ctx, L, d_descs + L.first);
+  } else if (impl == 1) {
+    if (L.tc_bn == 64) st = launch_tc_bn<64>(ctx, L, d_descs + L.first);
+    else if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, L, d_descs + L.first);
+    else st = launch_tc_bn<16>(ctx, L, d_descs + L.first);
   } else {
     dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
     if (L.big)
@@ -538,28 +584,33 @@ static fmmt_status launch_gemm(fmmt_op* op, const GemmLaunch& L) {
   return launch_gemm_group(ctx, L, op->d_descs, ctx->gemm_impl);
 }
 
-static int xy_ppc(const XYKernels& k) {
-  int ppc = fmmt::XY_THREADS / std::max(1, k.lines);
-  ppc = std::max(1, std::min(16, ppc));
+// Block shape of the xy FFT kernels: about one line per thread per pass, with
+// small CTAs (>= 64 threads, 1-2 planes) so that many CTAs are resident per
+// SM and the load / FFT / store phases of different CTAs overlap.
+static void xy_shape(const XYKernels& k, int* threads, int* ppc) {
+  int t = std::max(64, std::min(fmmt::XY_THREADS, ((k.lines + 31) / 32) * 32));
+  int p = std::max(1, std::min(2, t / std::max(1, k.lines)));
   const int64_t cap = (220 << 10) / 8 - FMMT_TW_NMAX;
-  while (ppc > 1 && (int64_t)ppc * k.plane_smem > cap) --ppc;
-  return ppc;
+  while (p > 1 && (int64_t)p * k.plane_smem > cap) --p;
+  *threads = t;
+  *ppc = p;
 }
 
 static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* out, int nplanes, float scale) {
   fmmt_ctx* ctx = op->ctx;
   XYKernels k = get_xy((int)op->n1, (int)op->n2);
   if (!k.fwd) return set_err(ctx, FMMT_E_UNSUPPORTED, "no xy kernel for n1=%lld n2=%lld", (long long)op->n1, (long long)op->n2);
-  const int ppc = xy_ppc(k);
+  int threads, ppc;
+  xy_shape(k, &threads, &ppc);
   const size_t smem = (size_t)(FMMT_TW_NMAX + (int64_t)ppc * k.plane_smem) * sizeof(float2);
   const unsigned grid = (unsigned)((nplanes + ppc - 1) / ppc);
   ProfScope ps(ctx, fwd ? "fft_fwd_xy" : "fft_inv_xy");
   if (fwd) {
-    FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)k.fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k.fwd<<<grid, fmmt::XY_THREADS, smem, ctx->stream>>>(in, out, nplanes, ppc);
+    FMMT_CUDA(ctx, set_smem_once((const void*)k.fwd, (int)smem));
+    k.fwd<<<grid, threads, smem, ctx->stream>>>(in, out, nplanes, ppc);
   } else {
-    FMMT_CUDA(ctx, cudaFuncSetAttribute((const void*)k.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k.inv<<<grid, fmmt::XY_THREADS, smem, ctx->stream>>>(in, out, nplanes, ppc, scale);
+    FMMT_CUDA(ctx, set_smem_once((const void*)k.inv, (int)smem));
+    k.inv<<<grid, threads, smem, ctx->stream>>>(in, out, nplanes, ppc, scale);
   }
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;
@@ -595,20 +646,35 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
 }
 
 template <int N3>
-static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, dim3 grid, const ZArgs& a) {
+static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
   using Cfg = fmmt::TcGemmCfg<(N3 < 16 ? 16 : N3)>;
   const void* fn = mode == fmmt::Z_RESTORE ? (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE>
                                            : (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK>;
-  FMMT_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  if (mode == fmmt::Z_RESTORE) fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
-  else fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
+  FMMT_CUDA(ctx, set_smem_once(fn, Cfg::SMEM));
+  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // persistent
+  if (mode == fmmt::Z_RESTORE) fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
+  else fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+template <int N3>
+static fmmt_status launch_tc1_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
+  using Cfg = fmmt::v1::TcGemmCfg<(N3 < 16 ? 16 : N3)>;
+  const void* fn = mode == fmmt::Z_RESTORE ? (const void*)fmmt::v1::k_tc_conv_z<N3, fmmt::Z_RESTORE>
+                                           : (const void*)fmmt::v1::k_tc_conv_z<N3, fmmt::Z_LOWRANK>;
+  FMMT_CUDA(ctx, set_smem_once(fn, Cfg::SMEM));
+  dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)nq);
+  if (mode == fmmt::Z_RESTORE) fmmt::v1::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
+  else fmmt::v1::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;
 }
 
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout) {
   fmmt_ctx* ctx = op->ctx;
-  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
+  if (ctx->gemm_impl >= 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
     fill_zargs(op, a);
     a.W = op->W + (int64_t)qoff * (op->n3 / 2) * a.n12;
@@ -616,13 +682,20 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     a.G = a.G + (int64_t)qoff * a.g_stride;
     if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
     a.Tout = Tout;
-    dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)nq);
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : "restore_conv_z");
+    if (ctx->gemm_impl == 2) {
+      switch (op->n3) {
+        case 4: return launch_tc1_z<4>(ctx, mode, nq, a);
+        case 8: return launch_tc1_z<8>(ctx, mode, nq, a);
+        case 16: return launch_tc1_z<16>(ctx, mode, nq, a);
+        default: return launch_tc1_z<32>(ctx, mode, nq, a);
+      }
+    }
     switch (op->n3) {
-      case 4: return launch_tc_z<4>(ctx, mode, grid, a);
-      case 8: return launch_tc_z<8>(ctx, mode, grid, a);
-      case 16: return launch_tc_z<16>(ctx, mode, grid, a);
-      default: return launch_tc_z<32>(ctx, mode, grid, a);
+      case 4: return launch_tc_z<4>(ctx, mode, nq, a);
+      case 8: return launch_tc_z<8>(ctx, mode, nq, a);
+      case 16: return launch_tc_z<16>(ctx, mode, nq, a);
+      default: return launch_tc_z<32>(ctx, mode, nq, a);
     }
   }
   ZKernel k = get_z((int)op->n3, mode);
@@ -692,6 +765,70 @@ static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void*
   return FMMT_OK;
 }
 
+// Run `body` (the launches of one matvec) through a CUDA graph: the second
+// call with the same buffers captures it, later calls replay it with one
+// cudaGraphLaunch (the hot path is otherwise bound by ~300 host-side kernel
+// launches per matvec).  Direct launches when profiling (per-kernel events) or
+// on the legacy default stream (not capturable).
+template <class F>
+static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, const void* k2, const void* k3, F&& body) {
+  fmmt_ctx* ctx = op->ctx;
+  if (ctx->stream == nullptr || !ctx->use_graphs) return body();
+  if (ctx->profiling) {
+    // per-kernel profile: capture the matvec with its event-record nodes and run it as one
+    // graph, so the events time the kernels back to back (not host launch gaps)
+    cudaGraph_t graph = nullptr;
+    FMMT_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    fmmt_status st = body();
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    ctx->prof_execs.push_back(exec);
+    FMMT_CUDA(ctx, cudaGraphLaunch(exec, ctx->stream));
+    return FMMT_OK;
+  }
+  fmmt_op::GraphEntry* ge = nullptr;
+  for (auto& g : op->graphs)
+    if (g.key[0] == k0 && g.key[1] == k1 && g.key[2] == k2 && g.key[3] == k3) ge = &g;
+  if (ge && ge->exec) {
+    FMMT_CUDA(ctx, cudaGraphLaunch(ge->exec, ctx->stream));
+    ctx->launches += ge->launches;
+    return FMMT_OK;
+  }
+  if (!ge) {   // first call: run directly (allocates lazily sized workspaces), remember the key
+    fmmt_op::GraphEntry e;
+    e.key[0] = k0; e.key[1] = k1; e.key[2] = k2; e.key[3] = k3;
+    e.calls = 1;
+    op->graphs.push_back(e);
+    return body();
+  }
+  cudaGraph_t graph = nullptr;
+  FMMT_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+  const int64_t l0 = ctx->launches;
+  fmmt_status st = body();
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (st) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  ge->exec = exec;
+  ge->launches = ctx->launches - l0;
+  FMMT_CUDA(ctx, cudaGraphLaunch(exec, ctx->stream));
+  return FMMT_OK;
+}
+
 // ============================================================== C ABI
 extern "C" {
 
@@ -727,6 +864,8 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   ctx->rank = rank;
   ctx->world = world;
   if (const char* e = getenv("FMMT_GEMM")) ctx->gemm_impl = (strcmp(e, "ffma") == 0) ? 0 : 1;
+  if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, 128);
@@ -803,7 +942,7 @@ fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_
 int64_t fmmt_launch_count(const fmmt_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl) {
-  if (!ctx || (impl != 0 && impl != 1)) return FMMT_E_ARG;
+  if (!ctx || impl < 0 || impl > 2) return FMMT_E_ARG;
   ctx->gemm_impl = impl;
   return FMMT_OK;
 }
@@ -811,7 +950,7 @@ fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl) {
 fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64_t k, int transA, int transB,
                             const fmmt_c64* A, int64_t lda, const fmmt_c64* B, int64_t ldb, fmmt_c64* C, int64_t ldc) {
   if (!ctx) return FMMT_E_ARG;
-  CHECK_ARG(ctx, impl == 0 || impl == 1, "impl must be 0 or 1");
+  CHECK_ARG(ctx, impl >= 0 && impl <= 4, "impl must be 0..4");
   CHECK_ARG(ctx, A && B && C, "null matrix");
   CHECK_SHAPE(ctx, m >= 1 && n >= 1 && k >= 1 && m < (1 << 30) && n < (1 << 30) && k < (1 << 30), "bad gemm dims");
   cudaSetDevice(ctx->device);
@@ -901,6 +1040,9 @@ fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs) {
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->stream);
   op->PB = std::min<int64_t>(dirs, op->ndir);
+  for (auto& g : op->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  op->graphs.clear();
   return build_plans(op);
 }
 
@@ -909,7 +1051,7 @@ fmmt_status fmmt_translate(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_ou
   fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
   if (st) return st;
   cudaSetDevice(op->ctx->device);
-  return translate_impl(op, sig_in, sig_out);
+  return run_graphed(op, sig_in, sig_out, nullptr, nullptr, [&] { return translate_impl(op, sig_in, sig_out); });
 }
 
 static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float* w, float2* sum_out) {
@@ -958,8 +1100,11 @@ fmmt_status fmmt_translate_sum(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* si
   fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
   if (st) return st;
   (void)K;
-  if ((st = translate_impl(op, sig_in, sig_out))) return st;
-  return dirsum_and_reduce(op, reinterpret_cast<const float2*>(sig_out), w, reinterpret_cast<float2*>(sum_out));
+  return run_graphed(op, sig_in, sig_out, w, sum_out, [&] {
+    fmmt_status s2 = translate_impl(op, sig_in, sig_out);
+    if (s2) return s2;
+    return dirsum_and_reduce(op, reinterpret_cast<const float2*>(sig_out), w, reinterpret_cast<float2*>(sum_out));
+  });
 }
 
 fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, const float* w_host, fmmt_c64* sum_out_host,

@@ -24,10 +24,13 @@ struct fmmt_ctx {
   std::string err;
   int64_t launches = 0;
   bool profiling = false;
-  int gemm_impl = 1;                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
+  int num_sms = 148;                // SM count of the device (persistent grids)
+  int gemm_impl = 1;
+  bool use_graphs = true;           // replay whole matvecs as CUDA graphs (see run_graphed)                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
   std::vector<fmmt_prof_entry> pending;
   std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
   std::vector<cudaEvent_t> event_pool;
+  std::vector<void*> prof_execs;    // cudaGraphExec_t of profiled matvecs (destroyed at flush)
   void* blas = nullptr;             // cublasHandle_t (setup only)
   void* solver = nullptr;           // cusolverDnHandle_t (setup only)
 };

@@ -186,10 +186,10 @@ class Context:
         return {names[i].decode(): (ms[i], la[i]) for i in range(min(64, cnt.value))}
 
     def set_gemm_impl(self, impl: str):
-        _check(fmmt_set_gemm_impl(self.h, {"ffma": 0, "tc": 1}[impl]), self.h, "fmmt_set_gemm_impl")
+        _check(fmmt_set_gemm_impl(self.h, {"ffma": 0, "tc": 1, "tc1": 2}[impl]), self.h, "fmmt_set_gemm_impl")
 
     def test_cgemm(self, impl: str, m, n, k, A, lda, B, ldb, Cout, ldc, transA=0, transB=0):
-        _check(fmmt_test_cgemm(self.h, {"ffma": 0, "tc": 1}[impl], m, n, k, transA, transB, _ptr(A), lda, _ptr(B), ldb,
+        _check(fmmt_test_cgemm(self.h, {"ffma": 0, "tc": 1, "tc1": 2}[impl], m, n, k, transA, transB, _ptr(A), lda, _ptr(B), ldb,
                                _ptr(Cout), ldc), self.h, "fmmt_test_cgemm")
 
     def build_operator(self, Nx, Ny, Nz, edge, k, L, khat: np.ndarray, out):
