@@ -88,7 +88,7 @@ def kernel_work(info: dict, fmt: str, ranks: np.ndarray, ndir: int):
         w["conv_z_dense"] = float(ndir * n * 8)           # bytes: the operator read once
     else:
         # restore (8 r flop/pt) + Hadamard (6) + pruned z-DFT pair (5 log2 n3) per padded point
-        w["restore_conv_z"] = float(np.sum(8.0 * n * rz)) + ndir * n * (6 + 5 * lg3)
+        w[f"restore_conv_z_{fmt}"] = float(np.sum(8.0 * n * rz)) + ndir * n * (6 + 5 * lg3)
     return w
 
 
@@ -383,7 +383,7 @@ def run_ours(args):
         "config": {"workload": workload_str(args.config, [(f, t) for f, t, _ in ops]),
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": f"direction-shard x{world}",
-                   "restore_gemm": {"tc": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate (persistent, warp-specialised)", "tc1": "tcgen05 kind::tf32, 3xTF32 (first design)", "ffma": "FP32 FFMA"}[args.gemm]},
+                   "restore_gemm": {"tc": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate", "tc1": "tcgen05 kind::tf32, 3xTF32 (first design)", "ffma": "FP32 FFMA"}[args.gemm]},
         "gpu_launches": int(launches),
         "roofline": {"bound": bound, "kernel": dname, "achieved": None if achieved is None else round(achieved, 3),
                      "peak": round(peak, 2), "unit": unit,

@@ -103,8 +103,8 @@ int64_t fmmt_launch_count(const fmmt_ctx* ctx);
 
 /* Implementation of the restore GEMMs (Figs. 3-4 contractions): 1 = tcgen05
  * tensor cores, kind::tf32 with the 3xTF32 split and FP32 accumulation,
- * persistent warp-specialised kernels (default); 2 = the first tcgen05 design
- * (non-persistent); 0 = FP32 FFMA kernel.  2 and 0 are kept for A/B
+ * operands copied asynchronously into the UMMA layout (default); 2 = the first
+ * tcgen05 design (register-staged operands); 0 = FP32 FFMA kernel.  2 and 0 are kept for A/B
  * measurement.  All are hand-written sm_100a kernels of this library; none is
  * a CPU path.                                                                */
 fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl);

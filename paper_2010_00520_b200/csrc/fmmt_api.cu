@@ -240,6 +240,10 @@ struct fmmt_op {
   int* d_rank = nullptr;                       // per direction z-stage rank (3D formats)
   float2* tbar1 = nullptr;                     // TT-4D: T1 = U1 . C1 (Fig. 4(a) step 1), n1 n2 x r2
   float2* E = nullptr;                         // H-Tucker: (C12 . C1234) x1 U1 x2 U2, n1 n2 x r34
+  float* tbar1_pk = nullptr;                   // T1 pre-split for the tensor-core z-stage (k_tc_pack_a)
+  float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
+  std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
+  int64_t pack_bytes = 0;
   // workspace
   int64_t PB = 0;
   float2 *W = nullptr, *H = nullptr, *Gw = nullptr, *Cw = nullptr, *Mw = nullptr, *Nw = nullptr,
@@ -291,6 +295,10 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->d_rank) cudaFree(op->d_rank);
   if (op->tbar1) cudaFree(op->tbar1);
   if (op->E) cudaFree(op->E);
+  if (op->tbar1_pk) cudaFree(op->tbar1_pk);
+  if (op->E_pk) cudaFree(op->E_pk);
+  for (auto pk : op->arr_pk)
+    if (pk) cudaFree(pk);
   for (auto& g : op->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (op->d_in_host) cudaFree(op->d_in_host);
@@ -400,6 +408,42 @@ static fmmt_status run_one_gemm(fmmt_ctx* ctx, const GemmDesc& d, int impl, cons
   return st;
 }
 
+// Pre-split a static A operand for the tensor-core kernels (k_tc_pack_a).  Synchronous.
+static fmmt_status pack_a(fmmt_op* op, const GemmDesc& d, float** out) {
+  fmmt_ctx* ctx = op->ctx;
+  const int64_t tiles_m = (d.m + fmmt::TC_BM - 1) / fmmt::TC_BM, nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
+  const int64_t floats = tiles_m * nkc * fmmt::TC_PACK_FLOATS;
+  if (cudaMalloc(out, floats * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return set_err(ctx, FMMT_E_NOMEM, "packed operand allocation (%lld B) failed", (long long)(floats * 4));
+  }
+  op->pack_bytes += floats * 4;
+  const int64_t work = tiles_m * fmmt::TC_BM * nkc * (fmmt::TC_BK / 2);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 16));
+  {
+    ProfScope ps(ctx, "pack_a");
+    fmmt::k_tc_pack_a<<<blocks, 256, 0, ctx->stream>>>(d, *out);
+  }
+  FMMT_CUDA(ctx, cudaGetLastError());
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMMT_OK;
+}
+
+// A descriptor whose A operand is factor array `ai` (static): attach the pre-split copy
+// (made once per op; skipped when packing is disabled or the kernel is not tcgen05).
+static fmmt_status with_packed_a(fmmt_op* op, int ai, GemmDesc& d) {
+  if (!op->ctx->pack_factors || op->ctx->gemm_impl != 1) return FMMT_OK;
+  if ((int)op->arr_pk.size() <= ai) op->arr_pk.resize(ai + 1, nullptr);
+  if (!op->arr_pk[ai]) {
+    fmmt_status st = pack_a(op, d, &op->arr_pk[ai]);
+    if (st) return st;
+  }
+  d.Ap = op->arr_pk[ai];
+  d.a_nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
+  return FMMT_OK;
+}
+
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
 static void tucker_chain(fmmt_op* op, Batch& b) {
@@ -481,8 +525,9 @@ static fmmt_status build_plans(fmmt_op* op) {
       case FMMT_TUCKER4D: {
         const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3);
         // a3 (Fig. 3(b)): C_q = C(r1 r2 r3 x r4) . U4[p,:]^T
-        add_gemm(op, b, {gd(op->arr[0], op->arr[4] + b.q0, op->Cw, r1 * r2 * r3, b.nq, r4, 1, r1 * r2 * r3, op->ndir, r1 * r2 * r3)},
-                 "slice_tucker4d");
+        GemmDesc ds = gd(op->arr[0], op->arr[4] + b.q0, op->Cw, r1 * r2 * r3, b.nq, r4, 1, r1 * r2 * r3, op->ndir, r1 * r2 * r3);
+        if ((st = with_packed_a(op, 0, ds))) return st;
+        add_gemm(op, b, {ds}, "slice_tucker4d");
         tucker_chain(op, b);
         break;
       }
@@ -494,10 +539,13 @@ static fmmt_status build_plans(fmmt_op* op) {
         const int64_t r3 = rk(op, 0, 2), r4 = rk(op, 0, 3), r34 = rk(op, 0, 5);
         const int64_t nq = b.nq;
         const float2 *U4 = op->arr[3], *C34 = op->arr[5];
-        add_gemm(op, b, {gdx(C34, U4 + b.q0, op->Mw, r3 * r34, nq, r4, 1, r3 * r4, r3, r3, op->ndir, 1, 1, r3 * nq, r3, r3)},
-                 "slice_htucker_M");
-        add_gemm(op, b, {gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12)},
-                 "slice_htucker_G");
+        GemmDesc dm = gdx(C34, U4 + b.q0, op->Mw, r3 * r34, nq, r4, 1, r3 * r4, r3, r3, op->ndir, 1, 1, r3 * nq, r3, r3);
+        if ((st = with_packed_a(op, 5, dm))) return st;
+        add_gemm(op, b, {dm}, "slice_htucker_M");
+        GemmDesc dg = gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12);
+        dg.Ap = op->E_pk;
+        dg.a_nkc = (int)((r34 + fmmt::TC_BK - 1) / fmmt::TC_BK);
+        add_gemm(op, b, {dg}, "slice_htucker_G");
         break;
       }
       case FMMT_TT3D: {
@@ -516,8 +564,9 @@ static fmmt_status build_plans(fmmt_op* op) {
       case FMMT_TT4D: {
         const int64_t r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
         // a3 (Fig. 4(b) step 1, columns of T2 for the batch): V_q = C2(r2 n3 x r3) . U_last[p,:]^T
-        add_gemm(op, b, {gd(op->arr[2], op->arr[3] + b.q0, op->Vw, r2 * n3, b.nq, r3, 1, r2 * n3, op->ndir, r2 * n3)},
-                 "slice_tt4d");
+        GemmDesc dv = gd(op->arr[2], op->arr[3] + b.q0, op->Vw, r2 * n3, b.nq, r3, 1, r2 * n3, op->ndir, r2 * n3);
+        if ((st = with_packed_a(op, 2, dv))) return st;
+        add_gemm(op, b, {dv}, "slice_tt4d");
         break;
       }
     }
@@ -535,9 +584,8 @@ template <int BN>
 static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
   using Cfg = fmmt::TcGemmCfg<BN>;
   FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN>, Cfg::SMEM));
-  const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // persistent
-  fmmt::k_tc_cgemm<BN><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, L.ndesc);
+  dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
+  fmmt::k_tc_cgemm<BN><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
   return FMMT_OK;
 }
 
@@ -551,7 +599,7 @@ static fmmt_status launch_tc1_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmD
 }
 
 // Launch one descriptor group.  impl: 0 = FP32 FFMA kernel, 1 = tcgen05 3xTF32
-// (persistent, warp-specialised), 2 = tcgen05 3xTF32 first design (A/B).
+// (cp.async into the UMMA layout, 2 MMAs per K-step), 2 = first tcgen05 design (A/B).
 static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d_descs, int impl) {
   if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
   fmmt_status st = FMMT_OK;
@@ -639,24 +687,39 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
       a.V = op->arr[2]; a.v_off = op->d_voff; a.v_sc = op->n3; a.v_sk = 1; a.rank_p = op->d_rank;
       break;
     case FMMT_TT4D:
-      a.G = op->tbar1; a.g_stride = 0;
+      a.G = op->tbar1; a.g_stride = 0; a.Gp = op->tbar1_pk;
       a.V = op->Vw; a.v_stride = rk(op, 0, 1) * op->n3; a.v_sc = 1; a.v_sk = rk(op, 0, 1); a.rank = (int)rk(op, 0, 1);
       break;
   }
 }
 
-template <int N3>
-static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  using Cfg = fmmt::TcGemmCfg<(N3 < 16 ? 16 : N3)>;
-  const void* fn = mode == fmmt::Z_RESTORE ? (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE>
-                                           : (const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK>;
-  FMMT_CUDA(ctx, set_smem_once(fn, Cfg::SMEM));
-  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // persistent
-  if (mode == fmmt::Z_RESTORE) fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
-  else fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, fmmt::TC_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
+template <int N3, int ND>
+static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
+  using Cfg = fmmt::TcGemmCfg<(N3 * ND < 16 ? 16 : N3 * ND)>;
+  dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)((nq + ND - 1) / ND));
+  if (mode == fmmt::Z_RESTORE) {
+    if constexpr (ND == 1) {
+      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1>, Cfg::SMEM));
+      fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, nq);
+    }
+  } else {
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND>, Cfg::SMEM));
+    fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, nq);
+  }
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;
+}
+
+// Directions per z tile: > 1 only when all directions share G (TT-4D's T1) and the
+// V_q of consecutive directions are contiguous ([q][kz][c]), up to 2 n3 = 64 columns.
+template <int N3>
+static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
+  const bool shareable = a.g_stride == 0 && !a.v_off && a.v_stride == (int64_t)N3 * a.v_sk && mode != fmmt::Z_RESTORE;
+  if (shareable && N3 <= 32 && ctx->z_multidir) {
+    constexpr int ND = 64 / N3 > 4 ? 4 : 64 / N3;
+    return launch_tc_z_nd<N3, ND>(ctx, mode, nq, a);
+  }
+  return launch_tc_z_nd<N3, 1>(ctx, mode, nq, a);
 }
 
 template <int N3>
@@ -682,7 +745,9 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     a.G = a.G + (int64_t)qoff * a.g_stride;
     if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
     a.Tout = Tout;
-    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : "restore_conv_z");
+    static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
+                                   "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
+    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
     if (ctx->gemm_impl == 2) {
       switch (op->n3) {
         case 4: return launch_tc1_z<4>(ctx, mode, nq, a);
@@ -865,6 +930,8 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   ctx->world = world;
   if (const char* e = getenv("FMMT_GEMM")) ctx->gemm_impl = (strcmp(e, "ffma") == 0) ? 0 : 1;
   if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
     ncclUniqueId id;
@@ -989,7 +1056,7 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
   info->compressed_bytes = comp * 8;
   info->original_bytes = op->n1 * op->n2 * op->n3 * op->ndir * 8;
   info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0) +
-                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0);
+                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0) + op->pack_bytes;
   info->batch = op->PB;
   // restore complex MACs per matvec (a3 + a4), in the contraction order the kernels use
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n = n1 * n2 * n3;
@@ -1267,31 +1334,23 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     cudaMemcpy(op->d_rank, rz.data(), ndir * sizeof(int), cudaMemcpyHostToDevice);
   }
   if (format == FMMT_HTUCKER4D) {
-    // Direction-independent part of Fig. 3(c), once per op:
-    //   D  = C12 (r1 r2 x r12) . C1234 (r12 x r34)
-    //   E1[i + n1 b + n1 r2 j] = sum_a D[a + r1 (b + r2 j)] U1[i + n1 a]
-    //   E [i + n1 jj + n12 j]  = sum_b E1[i + n1 b + n1 r2 j] U2[jj + n2 b]
+    // Direction-independent part of Fig. 3(c), once per op, in FP64 (setup):
+    //   E[i + n1 jj + n12 j] = sum_{a,b} U1[i,a] U2[jj,b] (C12 . C1234)[a + r1 b, j]
     const int64_t r1 = R(0, 0), r2 = R(0, 1), r12 = R(0, 4), r34 = R(0, 5), n12 = n1 * n2;
-    float2 *D = nullptr, *E1 = nullptr;
-    if (cudaMalloc(&op->E, n12 * r34 * sizeof(float2)) != cudaSuccess ||
-        cudaMalloc(&D, r1 * r2 * r34 * sizeof(float2)) != cudaSuccess ||
-        cudaMalloc(&E1, n1 * r2 * r34 * sizeof(float2)) != cudaSuccess) {
-      if (D) cudaFree(D);
+    if (cudaMalloc(&op->E, n12 * r34 * sizeof(float2)) != cudaSuccess) {
+      cudaGetLastError();
       fmmt_op_destroy(op);
       return set_err(ctx, FMMT_E_NOMEM, "H-Tucker E allocation failed");
     }
-    fmmt_status st = run_one_gemm(ctx, gd(op->arr[4], op->arr[6], D, r1 * r2, r34, r12, 0, r1 * r2, r12, r1 * r2), ctx->gemm_impl,
-                                  "htucker_D");
-    if (!st) st = run_one_gemm(ctx, gdx(D, op->arr[0], E1, r2 * r34, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, 0, NODIV, 1),
-                               ctx->gemm_impl, "htucker_E1");
-    if (!st) st = run_one_gemm(ctx, gdx(E1, op->arr[1], op->E, n1 * r34, n2, r2, 1, n1 * r2, n1, n1, n2, 1, 1, n12, n1, n1),
-                               ctx->gemm_impl, "htucker_E");
-    cudaError_t e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(D);
-    cudaFree(E1);
-    if (st || e != cudaSuccess) {
+    fmmt_status st = fmmt_internal::htucker_E_fp64(ctx, op->arr[0], op->arr[1], op->arr[4], op->arr[6], n1, n2, r1, r2,
+                                                   r12, r34, op->E);
+    if (st) {
       fmmt_op_destroy(op);
-      return st ? st : set_err(ctx, FMMT_E_CUDA, "H-Tucker E gemm failed: %s", cudaGetErrorString(e));
+      return st;
+    }
+    if ((st = pack_a(op, gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0), &op->E_pk))) {
+      fmmt_op_destroy(op);
+      return st;
     }
   }
   fmmt_status st = build_plans(op);
@@ -1300,30 +1359,24 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     return st;
   }
   if (format == FMMT_TT4D) {
-    // T1 = U1 . C1 (Fig. 4(a) step 1, reused by every direction of Fig. 4(b)), stored [b][ij]
+    // T1 = U1 . C1 (Fig. 4(a) step 1, reused by every direction of Fig. 4(b)), stored [b][ij], in FP64
     const int64_t r1 = R(0, 0), r2 = R(0, 1);
     if (cudaMalloc(&op->tbar1, n1 * n2 * r2 * sizeof(float2)) != cudaSuccess) {
+      cudaGetLastError();
       fmmt_op_destroy(op);
       return set_err(ctx, FMMT_E_NOMEM, "T1 allocation failed");
     }
-    Batch tmp;
-    const size_t first = op->descs.size();
-    add_gemm(op, tmp, {gd(op->arr[0], op->arr[1], op->tbar1, n1, n2 * r2, r1, 0, n1, r1, n1)}, "tt4d_T1");
-    GemmDesc* dd = nullptr;
-    cudaMalloc(&dd, sizeof(GemmDesc));
-    cudaMemcpy(dd, &op->descs[first], sizeof(GemmDesc), cudaMemcpyHostToDevice);
-    GemmLaunch L = tmp.gemms[0];
-    const int bm = L.big ? 64 : 32;
-    (void)bm;
-    dim3 grid((unsigned)L.maxtiles, 1, 1);
-    if (L.big) fmmt::k_cgemm<64, 64, 16, 4, 4><<<grid, 256, 0, ctx->stream>>>(dd);
-    else fmmt::k_cgemm<32, 32, 16, 4, 4><<<grid, 64, 0, ctx->stream>>>(dd);
-    cudaError_t e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(dd);
-    op->descs.resize(first);
-    if (e != cudaSuccess) {
+    fmmt_status tst = fmmt_internal::tt4d_T1_fp64(ctx, op->arr[0], op->arr[1], n1, r1, n2, r2, op->tbar1);
+    if (tst) {
       fmmt_op_destroy(op);
-      return set_err(ctx, FMMT_E_CUDA, "T1 gemm failed: %s", cudaGetErrorString(e));
+      return tst;
+    }
+    const int64_t n12 = n1 * n2;
+    fmmt_status pst = pack_a(op, gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0),
+                             &op->tbar1_pk);
+    if (pst) {
+      fmmt_op_destroy(op);
+      return pst;
     }
   }
   *out = op;

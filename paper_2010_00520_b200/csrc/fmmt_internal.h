@@ -26,7 +26,9 @@ struct fmmt_ctx {
   bool profiling = false;
   int num_sms = 148;                // SM count of the device (persistent grids)
   int gemm_impl = 1;
-  bool use_graphs = true;           // replay whole matvecs as CUDA graphs (see run_graphed)                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
+  bool use_graphs = true;
+  bool z_multidir = false;
+  bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)          // TT-4D z-stage: several directions per tile (1 CTA/SM; slower, A/B)           // replay whole matvecs as CUDA graphs (see run_graphed)                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
   std::vector<fmmt_prof_entry> pending;
   std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
   std::vector<cudaEvent_t> event_pool;
@@ -45,6 +47,12 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
                       int64_t narrays, fmmt_op** out);
 
 void setup_release(fmmt_ctx* ctx);   // free cuBLAS / cuSOLVER handles
+
+// FP64 (cuBLAS ZGEMM) direction-independent restore operands, rounded once to complex64.
+fmmt_status htucker_E_fp64(fmmt_ctx* ctx, const float2* U1, const float2* U2, const float2* C12, const float2* C1234,
+                           int64_t n1, int64_t n2, int64_t r1, int64_t r2, int64_t r12, int64_t r34, float2* E);
+fmmt_status tt4d_T1_fp64(fmmt_ctx* ctx, const float2* U1, const float2* C1, int64_t n1, int64_t r1, int64_t n2,
+                         int64_t r2, float2* T1);
 
 }  // namespace fmmt_internal
 

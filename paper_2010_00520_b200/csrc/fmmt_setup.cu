@@ -759,3 +759,78 @@ extern "C" fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t 
   return fmmt_internal::create_op(ctx, format, n1, n2, n3, dir_count, ranks.empty() ? nullptr : ranks.data(), arrs.data(),
                                   narr_of[format], op);
 }
+
+// ============================================================== FP64 derived operands (setup)
+// The direction-independent products the hot path reuses every matvec are
+// computed here in complex128 (cuBLAS ZGEMM) from the complex64 factors and
+// rounded once to complex64, so they add one rounding (6e-8) instead of the
+// 3xTF32 GEMM error to the restore chain:
+//   H-Tucker (Fig. 3(c)):  E = (C12 . C1234) x1 U1 x2 U2        stored E[i + n1 j + n1 n2 jj]
+//   TT-4D (Fig. 4(b) step 1 of Fig. 4(a)):  T1 = U1 . C1          stored T1[i + n1 (j + n2 b)]
+__global__ void k_c2z(const float2* __restrict__ a, double2* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = make_double2(a[i].x, a[i].y);
+}
+
+namespace {
+struct ZBuf {
+  double2* p = nullptr;
+  ~ZBuf() { if (p) cudaFree(p); }
+};
+fmmt_status zalloc_from(fmmt_ctx* ctx, ZBuf& b, const float2* src, int64_t n) {
+  if (cudaMalloc(&b.p, std::max<int64_t>(1, n) * sizeof(double2)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, FMMT_E_NOMEM, "setup allocation (%lld B) failed", (long long)(n * 16));
+  }
+  if (src) k_c2z<<<nblk(n), 256, 0, ctx->stream>>>(src, b.p, n);
+  return FMMT_OK;
+}
+}  // namespace
+
+fmmt_status fmmt_internal::htucker_E_fp64(fmmt_ctx* ctx, const float2* U1, const float2* U2, const float2* C12,
+                                          const float2* C1234, int64_t n1, int64_t n2, int64_t r1, int64_t r2,
+                                          int64_t r12, int64_t r34, float2* E) {
+  cublasHandle_t blas;
+  cusolverDnHandle_t sol;
+  SETUP_TRY(handles(ctx, &blas, &sol));
+  ZBuf u1, u2, c12, c1234, D, E1, Ez;
+  SETUP_TRY(zalloc_from(ctx, u1, U1, n1 * r1));
+  SETUP_TRY(zalloc_from(ctx, u2, U2, n2 * r2));
+  SETUP_TRY(zalloc_from(ctx, c12, C12, r1 * r2 * r12));
+  SETUP_TRY(zalloc_from(ctx, c1234, C1234, r12 * r34));
+  SETUP_TRY(zalloc_from(ctx, D, nullptr, r1 * r2 * r34));
+  SETUP_TRY(zalloc_from(ctx, E1, nullptr, n1 * r2 * r34));
+  SETUP_TRY(zalloc_from(ctx, Ez, nullptr, n1 * n2 * r34));
+  const zc one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+  // D (r1 r2 x r34) = C12 (r1 r2 x r12) . C1234 (r12 x r34)
+  SETUP_CUBLAS(ctx, cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)(r1 * r2), (int)r34, (int)r12, &one, (const zc*)c12.p,
+                                (int)(r1 * r2), (const zc*)c1234.p, (int)r12, &zero, (zc*)D.p, (int)(r1 * r2)));
+  // E1 (n1 x r2 r34) = U1 (n1 x r1) . D (r1 x r2 r34)
+  SETUP_CUBLAS(ctx, cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, (int)(r2 * r34), (int)r1, &one, (const zc*)u1.p,
+                                (int)n1, (const zc*)D.p, (int)r1, &zero, (zc*)E1.p, (int)n1));
+  // E(:,:,j) (n1 x n2) = E1(:,:,j) (n1 x r2) . U2^T (r2 x n2), for every j < r34
+  SETUP_CUBLAS(ctx, cublasZgemmStridedBatched(blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)n1, (int)n2, (int)r2, &one,
+                                              (const zc*)E1.p, (int)n1, n1 * r2, (const zc*)u2.p, (int)n2, 0, &zero,
+                                              (zc*)Ez.p, (int)n1, n1 * n2, (int)r34));
+  k_z2c<<<nblk(n1 * n2 * r34), 256, 0, ctx->stream>>>(Ez.p, E, n1 * n2 * r34);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "H-Tucker E (FP64) failed");
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_internal::tt4d_T1_fp64(fmmt_ctx* ctx, const float2* U1, const float2* C1, int64_t n1, int64_t r1,
+                                        int64_t n2, int64_t r2, float2* T1) {
+  cublasHandle_t blas;
+  cusolverDnHandle_t sol;
+  SETUP_TRY(handles(ctx, &blas, &sol));
+  ZBuf u1, c1, t1;
+  SETUP_TRY(zalloc_from(ctx, u1, U1, n1 * r1));
+  SETUP_TRY(zalloc_from(ctx, c1, C1, r1 * n2 * r2));
+  SETUP_TRY(zalloc_from(ctx, t1, nullptr, n1 * n2 * r2));
+  const zc one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+  // T1 (n1 x n2 r2) = U1 (n1 x r1) . C1 (r1 x n2 r2)
+  SETUP_CUBLAS(ctx, cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, (int)(n2 * r2), (int)r1, &one, (const zc*)u1.p,
+                                (int)n1, (const zc*)c1.p, (int)r1, &zero, (zc*)t1.p, (int)n1));
+  k_z2c<<<nblk(n1 * n2 * r2), 256, 0, ctx->stream>>>(t1.p, T1, n1 * n2 * r2);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return set_err(ctx, FMMT_E_CUDA, "TT-4D T1 (FP64) failed");
+  return FMMT_OK;
+}

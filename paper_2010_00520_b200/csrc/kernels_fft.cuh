@@ -307,6 +307,7 @@ struct ZArgs {
   int p0;                    // op-local index of the batch's first direction
   // low-rank factors: T_p[ij, k] = sum_c G_p[c][ij] * V_p(c, k)
   const float2* G;           // base
+  const float* Gp;           // G pre-split for the tensor-core kernel (shared G only), or nullptr
   int64_t g_stride;          // per batch-local q (0 = shared G)
   const float2* V;           // base
   const int64_t* v_off;      // per op direction p (elements) or nullptr

@@ -28,6 +28,10 @@ struct GemmDesc {
   int64_t c_s0, c_s1, c_sn;
   int c_div;
   int64_t sA, sB, sC;  // sub-batch strides (elements)
+  // optional pre-split A for the tensor-core kernel (kernels_tcgemm.cuh, k_tc_pack_a):
+  // tile (m/128, k-chunk) at Ap + (tile_m * a_nkc + chunk) * TC_PACK_FLOATS; nullptr = none
+  const float* Ap;
+  int a_nkc;
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {

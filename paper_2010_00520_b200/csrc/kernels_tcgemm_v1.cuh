@@ -157,7 +157,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     if (kc >= 2) {
       tc::mbar_wait(&bar[s], ((kc >> 1) - 1) & 1);
       tc::fence_after_sync();
-      tc_flush<BN>(twarp + s * 2 * NR, acc);    // chunk kc-2 -> registers; slot s is free again
+      v1::tc_flush<BN>(twarp + s * 2 * NR, acc);    // chunk kc-2 -> registers; slot s is free again
     }
     uint8_t* st = tcsm + s * Cfg::STAGE;
     uint8_t* aHi = st;
@@ -230,7 +230,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   for (int kc = (nk >= 2 ? nk - 2 : 0); kc < nk; ++kc) {
     tc::mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
     tc::fence_after_sync();
-    tc_flush<BN>(twarp + (kc & 1) * 2 * NR, acc);
+    v1::tc_flush<BN>(twarp + (kc & 1) * 2 * NR, acc);
   }
 }
 
@@ -277,9 +277,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_cgemm(const GemmDesc* __restrict_
   const float2* __restrict__ B = d.B + (int64_t)sub * d.sB;
   float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
 
-  const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
+  const uint32_t tmem = v1::tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
   float acc[NR];
-  tc_mainloop<BN, SPLIT>(d, A, B, m0, n0, tcsm, bar, tmem, acc);
+  v1::tc_mainloop<BN, SPLIT>(d, A, B, m0, n0, tcsm, bar, tmem, acc);
 
   // ---- epilogue: registers -> C (thread = row)
   const int gm = m0 + threadIdx.x;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_cgemm(const GemmDesc* __restrict_
       if (gn < d.n) C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
     }
   }
-  tc_teardown<Cfg::TMEM_COLS>(tmem);
+  v1::tc_teardown<Cfg::TMEM_COLS>(tmem);
 }
 
 }  // namespace v1
@@ -332,9 +332,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a) {
   const float2* A = a.G + (int64_t)q * a.g_stride;
   const float2* B = a.V + (a.v_off ? a.v_off[p] : (int64_t)q * a.v_stride);
 
-  const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
+  const uint32_t tmem = v1::tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
   float acc[2 * BN];
-  tc_mainloop<BN>(d, A, B, m0, 0, tcsm, bar, tmem, acc);
+  v1::tc_mainloop<BN>(d, A, B, m0, 0, tcsm, bar, tmem, acc);
 
   const int tid = threadIdx.x;
   const int64_t ij = m0 + tid;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a) {
       for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
     }
   }
-  tc_teardown<Cfg::TMEM_COLS>(tmem);
+  v1::tc_teardown<Cfg::TMEM_COLS>(tmem);
 }
 
 }  // namespace v1
