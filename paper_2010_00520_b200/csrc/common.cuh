@@ -29,7 +29,9 @@ template <> struct ILog2<1> { static constexpr int value = 0; };
 
 __host__ __device__ constexpr int bitrev(int i, int bits) {
   int r = 0;
-  for (int b = 0; b < bits; ++b) r = (r << 1) | ((i >> b) & 1);
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+    if (b < bits) r = (r << 1) | ((i >> b) & 1);
   return r;
 }
 

@@ -30,6 +30,24 @@ __device__ __forceinline__ float2 twmul(float2 b, int j) {
   return cmul(b, twc<SPAN, INV>(j));
 }
 
+// Radix-2 butterfly stages of span SPAN, 2 SPAN, ..., M (compile-time recursion, so
+// every index and twiddle is a constant: no local-memory arrays).
+template <int M, bool INV, int SPAN>
+__device__ __forceinline__ void fft_stages(float2 (&y)[M]) {
+  constexpr int half = SPAN / 2;
+#pragma unroll
+  for (int g = 0; g < M; g += SPAN) {
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      const float2 a = y[g + j];
+      const float2 b = twmul<SPAN, INV>(y[g + j + half], j);
+      y[g + j] = cadd(a, b);
+      y[g + j + half] = csub(a, b);
+    }
+  }
+  if constexpr (SPAN < M) fft_stages<M, INV, 2 * SPAN>(y);
+}
+
 // In-place M-point DFT of x (natural order in and out).
 // PRUNED: x[M/2 .. M) are known to be zero and are not read (the zero-padded
 // upper half of eq. (5)'s Toeplitz embedding).
@@ -55,31 +73,7 @@ __device__ __forceinline__ void fft_reg(float2 (&x)[M]) {
         y[2 * t + 1] = csub(a, b);
       }
     }
-#pragma unroll
-    for (int s = 2; s <= LG; ++s) {
-      const int span = 1 << s;
-      const int half = span >> 1;
-#pragma unroll
-      for (int g = 0; g < M; g += span) {
-#pragma unroll
-        for (int j = 0; j < half; ++j) {
-          float2 a = y[g + j];
-          float2 b;
-          // span is a compile-time constant after unrolling; dispatch on it
-          switch (span) {
-            case 4: b = twmul<4, INV>(y[g + j + half], j); break;
-            case 8: b = twmul<8, INV>(y[g + j + half], j); break;
-            case 16: b = twmul<16, INV>(y[g + j + half], j); break;
-            case 32: b = twmul<32, INV>(y[g + j + half], j); break;
-            case 64: b = twmul<64, INV>(y[g + j + half], j); break;
-            case 128: b = twmul<128, INV>(y[g + j + half], j); break;
-            default: b = twmul<256, INV>(y[g + j + half], j); break;
-          }
-          y[g + j] = cadd(a, b);
-          y[g + j + half] = csub(a, b);
-        }
-      }
-    }
+    if constexpr (M >= 4) fft_stages<M, INV, 4>(y);
 #pragma unroll
     for (int i = 0; i < M; ++i) x[i] = y[i];
   }

@@ -343,7 +343,7 @@ static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, con
   }
   L.big = (mmin >= 64 && nmin >= 64);
   const int bm = L.big ? 64 : 32, bn = L.big ? 64 : 32;
-  L.tc_bn = nmin >= 64 ? 64 : (nmin >= 32 ? 32 : 16);
+  L.tc_bn = nmin >= 32 ? 32 : 16;   // BN = 64 needs 512 TMEM columns (1 CTA / SM)
   for (auto& d : ds) {
     int tiles = ((d.m + bm - 1) / bm) * ((d.n + bn - 1) / bn);
     L.maxtiles = std::max(L.maxtiles, tiles);
@@ -580,12 +580,14 @@ static fmmt_status build_plans(fmmt_op* op) {
 }
 
 // ============================================================== launches
+constexpr int TC_G = 1;   // thread groups per tensor-core CTA (2 = 256 threads: measured slower)
+
 template <int BN>
 static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
-  using Cfg = fmmt::TcGemmCfg<BN>;
-  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN>, Cfg::SMEM));
+  using Cfg = fmmt::TcGemmCfg<BN, TC_G>;
+  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN, TC_G>, Cfg::SMEM));
   dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
-  fmmt::k_tc_cgemm<BN><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
+  fmmt::k_tc_cgemm<BN, TC_G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(d);
   return FMMT_OK;
 }
 
@@ -611,8 +613,7 @@ static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const G
     else if (L.tc_bn == 32) st = launch_tc1_bn<32>(ctx, L, d_descs + L.first);
     else st = launch_tc1_bn<16>(ctx, L, d_descs + L.first);
   } else if (impl == 1) {
-    if (L.tc_bn == 64) st = launch_tc_bn<64>(ctx, L, d_descs + L.first);
-    else if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, L, d_descs + L.first);
+    if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, L, d_descs + L.first);
     else st = launch_tc_bn<16>(ctx, L, d_descs + L.first);
   } else {
     dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
@@ -695,16 +696,18 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
 
 template <int N3, int ND>
 static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  using Cfg = fmmt::TcGemmCfg<(N3 * ND < 16 ? 16 : N3 * ND)>;
+  constexpr int BN = N3 * ND < 16 ? 16 : N3 * ND;
+  constexpr int G = 1;   // 2 = even/odd kz split over two thread groups (measured slower: 1 CTA/SM by registers)
+  using Cfg = fmmt::TcGemmCfg<BN, G>;
   dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)((nq + ND - 1) / ND));
   if (mode == fmmt::Z_RESTORE) {
     if constexpr (ND == 1) {
-      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1>, Cfg::SMEM));
-      fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, nq);
+      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G>, Cfg::SMEM));
+      fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(a, nq);
     }
   } else {
-    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND>, Cfg::SMEM));
-    fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, nq);
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND, G>, Cfg::SMEM));
+    fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND, G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(a, nq);
   }
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;

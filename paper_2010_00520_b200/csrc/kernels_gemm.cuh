@@ -32,6 +32,7 @@ struct GemmDesc {
   // tile (m/128, k-chunk) at Ap + (tile_m * a_nkc + chunk) * TC_PACK_FLOATS; nullptr = none
   const float* Ap;
   int a_nkc;
+  int b_eo;            // tensor-core z-stage: B columns taken in (even, odd) order
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {

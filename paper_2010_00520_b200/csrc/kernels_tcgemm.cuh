@@ -9,10 +9,14 @@
 //   z-stage           T_p[ij,:] = G_p[ij,:] . V_p  fused with the z-DFT,
 //                     Hadamard product and inverse z-DFT          (a4-a6, eq. (5))
 //
-// One CTA = 128 threads = one 128-row x BN-column output tile (2 CTAs / SM for
-// BN <= 32).  Per K-chunk (TC_BK complex), double-buffered:
+// One CTA = 128*G threads computes one 128-row x BN-column output tile; the G
+// thread groups share the rows (thread = row tid % 128) and split the columns
+// (group tid / 128 owns columns [g BN/G, (g+1) BN/G)), so the per-chunk work
+// (operand conversion, TMEM drain) is spread over 4G warps.  Per K-chunk
+// (TC_BK complex), double-buffered:
 //   * cp.async copies the raw complex64 A elements straight into the canonical
-//     K-major UMMA layout, and the B elements into a small raw staging area;
+//     K-major UMMA layout (or, for pre-split static operands, one bulk async
+//     copy brings A_hi and A_lo), and the B elements into a raw staging area;
 //   * the threads round A in place to A_hi = rna_tf32(x), write A_lo =
 //     rna_tf32(x - A_hi) next to it, and build B' = [B^_hi ; B^_lo] (the
 //     complex-embedding rows, hi rows then lo rows).  (The tensor core reads the
@@ -30,78 +34,86 @@
 namespace fmmt {
 
 constexpr int TC_BM = 128;      // rows per tile (UMMA M)
-constexpr int TC_BK = 16;       // complex K per chunk (32 real = 4 UMMA K-steps)
-constexpr int TC_PACK_FLOATS = 2 * TC_BM * 2 * TC_BK;   // one packed A tile: hi + lo, 128 x 32 real
-constexpr int TC_FC = 1;        // chunks per TMEM flush group (4 K-steps per accumulator chain; 2 fails the 1e-6 restore bar)
+constexpr int TC_BK = 8;        // complex K per chunk (16 real = 2 UMMA K-steps)
+constexpr int TC_NS = 3;        // operand ring stages (MMAs of chunk k-1 overlap the conversion of chunk k)
+constexpr int TC_PACK_FLOATS = 2 * TC_BM * 2 * TC_BK;   // one packed A tile: hi + lo, 128 x 16 real
+constexpr int TC_FC = 2;        // chunks per TMEM flush group (4 K-steps per accumulator chain; 8 fails the 1e-6 restore bar)
 
-template <int BN>
+template <int BN, int G = 1>
 struct TcGemmCfg {
+  static constexpr int NT = 128 * G;                // threads
   static constexpr int NR = 2 * BN;                 // real N of C (re, im interleaved)
+  static constexpr int NRG = NR / G;                // real columns per thread group
   static constexpr int KR = 2 * TC_BK;              // real K per chunk
   static constexpr int A_BYTES = TC_BM * KR * 4;    // one of hi / lo (16 KB)
   static constexpr int BP_ROWS = 2 * NR;            // B' = [B^_hi ; B^_lo]
   static constexpr int BP_BYTES = BP_ROWS * KR * 4;
-  static constexpr int BITEMS = BN * (TC_BK / 2) / 128 > 0 ? BN * (TC_BK / 2) / 128 : 1;
-  static constexpr int BRAW = BITEMS * 128 * 16;    // raw B staging
+  static constexpr int BITEMS = BN * (TC_BK / 2) / NT > 0 ? BN * (TC_BK / 2) / NT : 1;
+  static constexpr int BRAW = BITEMS * NT * 16;     // raw B staging
   static constexpr int STAGE = 2 * A_BYTES + BP_BYTES + BRAW;
-  static constexpr int SMEM = 2 * STAGE;
+  static constexpr int SMEM = TC_NS * STAGE;
   // two accumulator slots (alternating K-chunks) x {hi.hi, hi.lo + lo.hi}
   static constexpr int TMEM_COLS = 4 * NR < 32 ? 32 : 4 * NR;
   static constexpr uint32_t LBO_A = TC_BM * 16;     // K-adjacent core matrices
   static constexpr uint32_t LBO_B = BP_ROWS * 16;
   static_assert(2 * NR <= 256, "UMMA N <= 256");
+  static_assert(NRG % 16 == 0, "TMEM drain granularity: 16 columns per thread group");
+  static_assert(TC_BK == 8, "copy mappings below assume 4 complex pairs per row and chunk");
 };
 
 // Accuracy of the tensor-core accumulation.  The tensor core adds each MMA's
 // products into the FP32 accumulator with truncation, so the error of one
 // accumulator grows with the number of MMAs chained into it (measured 2.4e-6
 // relative at K = 169 with a single chain, ~3.8e-8 per chained MMA; the
-// restore bound is 1e-6).  Each group of TC_FC K-chunks (8 K-steps) therefore
-// accumulates into a fresh TMEM slot, with the hi.hi products and the
-// 2^-11-smaller cross terms in separate accumulators, and the group results
-// are summed by the threads in FP32 registers (round-to-nearest).  Two slots
-// alternate so the next group's MMAs overlap the drain of the previous one.
-template <int BN>
-__device__ __forceinline__ void tc_flush(uint32_t tslot_addr, float (&acc)[2 * BN]) {
-  constexpr int NR = 2 * BN;
+// restore bound is 1e-6).  Each K-chunk (4 K-steps) therefore accumulates into
+// a fresh TMEM slot, with the hi.hi products and the 2^-11-smaller cross terms
+// in separate accumulators, and the chunk results are summed in FP32 registers
+// (round-to-nearest).  Two slots alternate so chunk k+1's MMAs overlap the
+// drain of chunk k.  A thread drains its row's columns [c0, c0 + NRG).
+template <int NR, int NRG>
+__device__ __forceinline__ void tc_flush(uint32_t tslot_addr, int c0, float (&acc)[NRG]) {
 #pragma unroll
-  for (int c0 = 0; c0 < NR; c0 += 16) {
+  for (int c = 0; c < NRG; c += 16) {
     float vm[16], vx[16];
-    tc::tmem_ld16(tslot_addr + c0, vm);
-    tc::tmem_ld16(tslot_addr + NR + c0, vx);
+    tc::tmem_ld16(tslot_addr + c0 + c, vm);
+    tc::tmem_ld16(tslot_addr + NR + c0 + c, vx);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[c0 + j] += vm[j] + vx[j];
+    for (int j = 0; j < 16; ++j) acc[c + j] += vm[j] + vx[j];
   }
 }
 
-// acc[2BN] (registers, thread = row m0 + tid) = A[m0:m0+128, :] . B[:, n0:n0+BN]
-// over all of K.  Called by all 128 threads.
-template <int BN>
+// acc[NRG] (registers; thread = row m0 + tid % 128, columns [g NRG, (g+1) NRG) of
+// the tile, re/im interleaved) = A[m0:m0+128, :] . B[:, n0:n0+BN] over all of K.
+// Called by all 128 G threads.  bar[0..1]: MMA commits per stage; bar[2..3]:
+// packed-A bulk copies per stage.
+template <int BN, int G>
 __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
                                             const float2* __restrict__ B, int m0, int n0, uint8_t* tcsm,
-                                            uint64_t* bar, uint32_t tmem, float (&acc)[2 * BN]) {
-  // bar[0..1]: MMA commits per stage; bar[2..3]: packed-A bulk copies per stage
-  using Cfg = TcGemmCfg<BN>;
-  constexpr int BM = TC_BM, BK = TC_BK, NR = Cfg::NR;
+                                            uint64_t* bar, uint32_t tmem,
+                                            float (&acc)[TcGemmCfg<BN, G>::NRG]) {
+  using Cfg = TcGemmCfg<BN, G>;
+  constexpr int BM = TC_BM, BK = TC_BK, NR = Cfg::NR, NRG = Cfg::NRG, NT = Cfg::NT;
   constexpr int BITEMS = Cfg::BITEMS;
   const uint32_t sbase = tc::smem_u32(tcsm);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, row = tid & 127, grp = tid >> 7;
+  const int wrow = row >> 5, lane = tid & 31;      // warp index within the group = TMEM lane quarter
   const bool a_kcontig = d.a_sk == 1;   // rows of A are contiguous in K
   const bool b_kcontig = d.b_sk == 1;
-  // rows this thread copies: row-per-thread (row tid) or K-contiguous (4 rows)
+  // rows this thread copies: row-per-thread (row) or K-contiguous (4 rows)
   int64_t arow[4];
   bool okrow[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int r = a_kcontig ? (lane & 7) + 8 * (u + 4 * warp) : tid;
+    const int r = a_kcontig ? (lane & 7) + 8 * (u + 4 * wrow) : row;
     okrow[u] = m0 + r < d.m;
     arow[u] = okrow[u] ? a_row(d, m0 + r) : 0;
   }
   constexpr uint32_t IDESC_BP = tc::idesc_tf32(BM, 2 * NR);   // A_hi x [B_hi ; B_lo]
   constexpr uint32_t IDESC_B = tc::idesc_tf32(BM, NR);        // A_lo x B_hi
 #pragma unroll
-  for (int j = 0; j < NR; ++j) acc[j] = 0.f;
-  const uint32_t twarp = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
+  for (int j = 0; j < NRG; ++j) acc[j] = 0.f;
+  const uint32_t twarp = tmem + ((uint32_t)(wrow * 32) << 16);   // this warp's TMEM lanes
+  const int c0 = grp * NRG;                                      // this group's columns
 
   const int nk = (d.k + BK - 1) / BK;
   const bool apack = d.Ap != nullptr;   // A pre-split into hi/lo tiles: one bulk copy per chunk
@@ -109,59 +121,73 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
   auto issue = [&](int c) {
     const int k0 = c * BK;
-    const uint32_t st = sbase + (c & 1) * Cfg::STAGE;
+    const uint32_t st = sbase + (c % TC_NS) * Cfg::STAGE;
     if (apack) {
       if (tid == 0) {
-        tc::mbar_expect_tx(&bar[2 + (c & 1)], 2 * Cfg::A_BYTES);
-        tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[2 + (c & 1)]);
+        tc::mbar_expect_tx(&bar[TC_NS + (c % TC_NS)], 2 * Cfg::A_BYTES);
+        tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[TC_NS + (c % TC_NS)]);
       }
     } else if (!a_kcontig) {
+      // row-per-thread: group g copies K elements [g BK/G, (g+1) BK/G) of its row
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
+      for (int kq = 0; kq < BK / G; ++kq) {
+        const int kk = grp * (BK / G) + kq;
         const int gk = k0 + kk;
         const bool ok = okrow[0] && gk < d.k;
-        tc::cp_async8(st + tid * 16 + (kk >> 1) * Cfg::LBO_A + (kk & 1) * 8,
+        tc::cp_async8(st + row * 16 + (kk >> 1) * Cfg::LBO_A + (kk & 1) * 8,
                       ok ? (const void*)(A + arow[0] + gk * d.a_sk) : (const void*)A, ok);
       }
     } else {
+      // K-contiguous rows: lane -> (row low 3 bits, complex pair kp = lane / 8); item u = 0..3 -> row
+      // group (u + 4 * warp); thread group g takes items u % G == g
 #pragma unroll
-      for (int i = 0; i < BK / 2; ++i) {
-        const int kp = (lane >> 3) + 4 * (i & 1);
-        const int r = (lane & 7) + 8 * ((i >> 1) + 4 * warp);
+      for (int uu = 0; uu < 4 / G; ++uu) {
+        const int u = uu * G + grp;
+        const int kp = lane >> 3;
+        const int r = (lane & 7) + 8 * (u + 4 * wrow);
         const int gk = k0 + 2 * kp;
-        const bool ok0 = okrow[i >> 1] && gk < d.k, ok1 = okrow[i >> 1] && gk + 1 < d.k;
+        const bool okr = (G == 1) ? okrow[uu] : (grp ? okrow[2 * uu + 1] : okrow[2 * uu]);
+        const int64_t ar = (G == 1) ? arow[uu] : (grp ? arow[2 * uu + 1] : arow[2 * uu]);
+        const bool ok0 = okr && gk < d.k, ok1 = okr && gk + 1 < d.k;
         const uint32_t dst = st + r * 16 + kp * Cfg::LBO_A;
-        tc::cp_async8(dst, ok0 ? (const void*)(A + arow[i >> 1] + gk) : (const void*)A, ok0);
-        tc::cp_async8(dst + 8, ok1 ? (const void*)(A + arow[i >> 1] + gk + 1) : (const void*)A, ok1);
+        tc::cp_async8(dst, ok0 ? (const void*)(A + ar + gk) : (const void*)A, ok0);
+        tc::cp_async8(dst + 8, ok1 ? (const void*)(A + ar + gk + 1) : (const void*)A, ok1);
       }
     }
     const uint32_t rb = st + 2 * Cfg::A_BYTES + Cfg::BP_BYTES;
 #pragma unroll
     for (int i = 0; i < BITEMS; ++i) {
-      const int idx = tid + 128 * i;
+      const int idx = tid + NT * i;
       int j, kp;
       if (!b_kcontig) { j = idx % BN; kp = idx / BN; }    // n (not k) contiguous in memory
       else { kp = idx % (BK / 2); j = idx / (BK / 2); }   // k contiguous
       const int gn = n0 + j, gk = k0 + 2 * kp;
       const bool okn = idx < BN * (BK / 2) && gn < d.n;
+      const int gc = d.b_eo ? (gn < d.n / 2 ? 2 * gn : 2 * (gn - d.n / 2) + 1) : gn;   // even/odd column order
       const bool ok0 = okn && gk < d.k, ok1 = okn && gk + 1 < d.k;
-      const uint32_t dst = rb + (i * 128 + tid) * 16;
-      tc::cp_async8(dst, ok0 ? (const void*)(B + gk * d.b_sk + gn * d.b_sn) : (const void*)B, ok0);
-      tc::cp_async8(dst + 8, ok1 ? (const void*)(B + (gk + 1) * d.b_sk + gn * d.b_sn) : (const void*)B, ok1);
+      const uint32_t dst = rb + (i * NT + tid) * 16;
+      tc::cp_async8(dst, ok0 ? (const void*)(B + gk * d.b_sk + gc * d.b_sn) : (const void*)B, ok0);
+      tc::cp_async8(dst + 8, ok1 ? (const void*)(B + (gk + 1) * d.b_sk + gc * d.b_sn) : (const void*)B, ok1);
     }
     tc::cp_async_commit();
   };
 
+  // bar[0 .. TC_NS): MMA commit of the chunk in stage s; bar[TC_NS .. 2 TC_NS): packed-A copies.
+  // Chunk c uses stage c % TC_NS (phase (c / TC_NS) & 1 of its barriers) and TMEM slot
+  // (c / TC_FC) & 1.
+  int flushed = 0;                       // flush groups already drained into acc
+  auto drain_complete = [&](int done) {  // chunks [0, done) have completed MMAs
+    for (; (flushed + 1) * TC_FC <= done; ++flushed)
+      tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+  };
   issue(0);
   for (int kc = 0; kc < nk; ++kc) {
-    const int s = kc & 1;
-    const bool group_done = kc >= 1 && kc % TC_FC == 0;   // chunk kc-1 closed a flush group
-    if (kc >= 1 && (kc + 1 < nk || group_done)) {
-      // the MMAs of chunk kc-1 (and all earlier) are complete: stage s^1 is free and a closed
-      // group's TMEM slot can be drained
-      tc::mbar_wait(&bar[s ^ 1], ((kc - 1) >> 1) & 1);
+    const int s = kc % TC_NS;
+    if (kc >= 2) {
+      // MMAs of chunk kc-2 (and earlier) complete: stage (kc+1) % NS is free, closed groups drain
+      tc::mbar_wait(&bar[(kc - 2) % TC_NS], ((kc - 2) / TC_NS) & 1);
       tc::fence_after_sync();
-      if (group_done) tc_flush<BN>(twarp + (((kc - 1) / TC_FC) & 1) * 2 * NR, acc);
+      drain_complete(kc - 1);
     }
     if (kc + 1 < nk) {
       issue(kc + 1);
@@ -169,10 +195,10 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     } else {
       tc::cp_async_wait<0>();
     }
-    if (apack) tc::mbar_wait(&bar[2 + s], (kc >> 1) & 1);   // packed A of chunk kc has landed
+    if (apack) tc::mbar_wait(&bar[TC_NS + s], (kc / TC_NS) & 1);   // packed A of chunk kc has landed
     __syncthreads();                                 // chunk kc's A_hi (all threads' copies) is in place
     uint8_t* st = tcsm + s * Cfg::STAGE;
-    const uint8_t* aHi = st;
+    uint8_t* aHi = st;
     uint8_t* aLo = st + Cfg::A_BYTES;
     uint8_t* bP = st + 2 * Cfg::A_BYTES;
     const uint8_t* bRaw = bP + Cfg::BP_BYTES;
@@ -180,27 +206,29 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     //      (same canonical offsets).  Round-to-nearest on both parts keeps |x - hi - lo| and the
     //      dropped lo.lo product at 2^-22 |x| (truncated hi doubles both: measured restore errors
     //      up to 1.02e-6 against the 1e-6 bar).
+    if (!apack) {
 #pragma unroll
-    for (int i = 0; i < (apack ? 0 : Cfg::A_BYTES / (16 * 128)); ++i) {
-      const uint32_t off = (i * 128 + tid) * 16;
-      const float4 a = *reinterpret_cast<const float4*>(aHi + off);
-      float4 hi, lo;
-      tc::split_tf32(a.x, hi.x, lo.x);
-      tc::split_tf32(a.y, hi.y, lo.y);
-      tc::split_tf32(a.z, hi.z, lo.z);
-      tc::split_tf32(a.w, hi.w, lo.w);
-      *reinterpret_cast<float4*>(const_cast<uint8_t*>(aHi) + off) = hi;
-      *reinterpret_cast<float4*>(aLo + off) = lo;
+      for (int i = 0; i < Cfg::A_BYTES / (16 * NT); ++i) {
+        const uint32_t off = (i * NT + tid) * 16;
+        const float4 a = *reinterpret_cast<const float4*>(aHi + off);
+        float4 hi, lo;
+        tc::split_tf32(a.x, hi.x, lo.x);
+        tc::split_tf32(a.y, hi.y, lo.y);
+        tc::split_tf32(a.z, hi.z, lo.z);
+        tc::split_tf32(a.w, hi.w, lo.w);
+        *reinterpret_cast<float4*>(aHi + off) = hi;
+        *reinterpret_cast<float4*>(aLo + off) = lo;
+      }
     }
     // ---- B' rows: [0, NR) = B^_hi, [NR, 2NR) = B^_lo;  row 2j = [Re b, -Im b], row 2j+1 = [Im b, Re b]
 #pragma unroll
     for (int i = 0; i < BITEMS; ++i) {
-      const int idx = tid + 128 * i;
+      const int idx = tid + NT * i;
       if (idx >= BN * (BK / 2)) continue;
       int j, kp;
       if (!b_kcontig) { j = idx % BN; kp = idx / BN; }
       else { kp = idx % (BK / 2); j = idx / (BK / 2); }
-      const float4 bb = *reinterpret_cast<const float4*>(bRaw + (i * 128 + tid) * 16);
+      const float4 bb = *reinterpret_cast<const float4*>(bRaw + (i * NT + tid) * 16);
       const float4 r0 = make_float4(bb.x, -bb.y, bb.z, -bb.w);
       const float4 r1 = make_float4(bb.y, bb.x, bb.w, bb.z);
       const uint32_t off = (2 * j) * 16 + kp * Cfg::LBO_B;
@@ -222,7 +250,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
       const uint32_t sb = sa_hi + 2 * Cfg::A_BYTES;
       const uint32_t tm = tmem + ((kc / TC_FC) & 1) * 2 * NR, tx = tm + NR;
-      const bool fresh = kc % TC_FC == 0;              // first chunk of a flush group
+      const bool fresh = kc % TC_FC == 0;              // first chunk of a flush group (slot freed at kc-1)
 #pragma unroll
       for (int ks = 0; ks < Cfg::KR / 8; ++ks) {
         const uint64_t ah = tc::sdesc(sa_hi + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
@@ -234,10 +262,11 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       tc::mma_commit(&bar[s]);
     }
   }
-  // drain the last (open) flush group
-  tc::mbar_wait(&bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  // drain the remaining flush groups (the last one possibly partial)
+  tc::mbar_wait(&bar[(nk - 1) % TC_NS], ((nk - 1) / TC_NS) & 1);
   tc::fence_after_sync();
-  tc_flush<BN>(twarp + (((nk - 1) / TC_FC) & 1) * 2 * NR, acc);
+  drain_complete(nk);
+  if (flushed * TC_FC < nk) tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
 }
 
 // TMEM allocation + stage barriers (all threads call; warp 0 allocates).
@@ -246,7 +275,7 @@ __device__ __forceinline__ uint32_t tc_setup(uint64_t* bar, uint32_t* tslot) {
   if ((threadIdx.x >> 5) == 0) tc::tmem_alloc<TMEM_COLS>(tslot);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tc::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 2 * TC_NS; ++i) tc::mbar_init(&bar[i], 1);
     tc::fence_barrier_init();
   }
   tc::fence_before_sync();
@@ -262,12 +291,12 @@ __device__ __forceinline__ void tc_teardown(uint32_t tmem) {
   if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-template <int BN>
-__global__ void __launch_bounds__(128, 1) k_tc_cgemm(const GemmDesc* __restrict__ descs) {
-  using Cfg = TcGemmCfg<BN>;
-  constexpr int BM = TC_BM, NR = Cfg::NR;
+template <int BN, int G>
+__global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict__ descs) {
+  using Cfg = TcGemmCfg<BN, G>;
+  constexpr int BM = TC_BM, NRG = Cfg::NRG;
   extern __shared__ __align__(1024) uint8_t tcsm[];
-  __shared__ __align__(8) uint64_t bar[4];
+  __shared__ __align__(8) uint64_t bar[2 * TC_NS];
   __shared__ uint32_t tslot;
 
   const GemmDesc d = descs[blockIdx.z];
@@ -284,15 +313,16 @@ __global__ void __launch_bounds__(128, 1) k_tc_cgemm(const GemmDesc* __restrict_
   float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
 
   const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
-  float acc[NR];
-  tc_mainloop<BN>(d, A, B, m0, n0, tcsm, bar, tmem, acc);
+  float acc[NRG];
+  tc_mainloop<BN, G>(d, A, B, m0, n0, tcsm, bar, tmem, acc);
 
-  const int gm = m0 + threadIdx.x;
+  const int gm = m0 + (threadIdx.x & 127);
+  const int nb = n0 + (threadIdx.x >> 7) * (BN / G);
   if (gm < d.m) {
     const int64_t crow = c_row(d, gm);
 #pragma unroll
-    for (int j = 0; j < BN; ++j) {
-      const int gn = n0 + j;
+    for (int j = 0; j < BN / G; ++j) {
+      const int gn = nb + j;
       if (gn < d.n) C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
     }
   }
@@ -303,21 +333,27 @@ __global__ void __launch_bounds__(128, 1) k_tc_cgemm(const GemmDesc* __restrict_
 // Tensor-core version of k_conv_z (kernels_fft.cuh) for n3 <= 32: per batch
 // directions q0 .. q0+ND-1 and 128 (kx,ky) lines ij, the last restore contraction
 //     T_p[ij, kz] = sum_c G_q[c][ij] V_p(c, kz)        (a4: x3 U3 / TT tail)
-// runs on tcgen05 (3xTF32); the thread that owns line ij then does, per
+// runs on tcgen05 (3xTF32); the thread(s) owning line ij then do, per
 // direction, the pruned forward z-DFT of the half-padded spectrum W, the
 // Hadamard product with T_p (a5) and the inverse z-DFT truncated to z < Nz
-// (a6), in registers.  T_p never leaves the SM.  ND > 1 only when G is shared
-// by all directions (TT-4D: G = T1 of Fig. 4(b)) and V_q is laid out
-// [q][kz][c], so that one tile's B operand is ND directions' V side by side.
-template <int N3, int MODE, int ND>
-__global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a, int nq) {
+// (a6), in registers.  T_p never leaves the SM.
+//   G = 2 (n3 = 16, 32): the two thread groups take the even and the odd kz
+//   (B's columns are ordered even kz first): with x the Nz nonzero inputs,
+//     A^[2m]   = DFT_{n3/2}(x)[m],            A^[2m+1] = DFT_{n3/2}(x W_n3^z)[m],
+//     y[z]     = IDFT_{n3/2}(T_even A^_even)[z] + W_n3^{-z} IDFT_{n3/2}(T_odd A^_odd)[z],
+//   and the two halves of y are added through shared memory.
+//   ND > 1 only when G is shared by all directions (TT-4D: G = T1 of Fig. 4(b))
+//   and V_q is laid out [q][kz][c] (one tile's B = ND directions side by side).
+template <int N3, int MODE, int ND, int G>
+__global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
   constexpr int BN0 = N3 * ND;
   constexpr int BN = BN0 < 16 ? 16 : BN0;
-  using Cfg = TcGemmCfg<BN>;
+  using Cfg = TcGemmCfg<BN, G>;
   constexpr int Nz = N3 / 2;
   static_assert(ND == 1 || MODE != Z_RESTORE, "restore hook is per direction");
+  static_assert(G == 1 || (ND == 1 && BN == N3), "column groups split one direction's kz");
   extern __shared__ __align__(1024) uint8_t tcsm[];
-  __shared__ __align__(8) uint64_t bar[4];
+  __shared__ __align__(8) uint64_t bar[2 * TC_NS];
   __shared__ uint32_t tslot;
 
   const int q0 = blockIdx.y * ND;
@@ -331,6 +367,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a, int nq) {
   d.batch = 1;
   d.a_s0 = 1; d.a_s1 = 0; d.a_div = 1 << 30; d.a_sk = a.n12;
   d.b_sk = a.v_sc; d.b_sn = a.v_sk;     // ND > 1: v_stride == N3 * v_sk (checked on the host)
+  d.b_eo = (G == 2) ? 1 : 0;
   d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
   d.sA = d.sB = d.sC = 0;
   d.Ap = a.Gp;                          // pre-split shared G (TT-4D T1), or nullptr
@@ -338,19 +375,24 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a, int nq) {
   const float2* A = a.G + (int64_t)q0 * a.g_stride;
   const float2* B = a.V + (a.v_off ? a.v_off[p0] : (int64_t)q0 * a.v_stride);
 
-  const int64_t ij = m0 + threadIdx.x;
+  const int row = threadIdx.x & 127, grp = threadIdx.x >> 7;
+  const int64_t ij = m0 + row;
   const bool valid = ij < a.n12;
 
   const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
-  float acc[2 * BN];
-  tc_mainloop<BN>(d, A, B, m0, 0, tcsm, bar, tmem, acc);
+  float acc[Cfg::NRG];
+  tc_mainloop<BN, G>(d, A, B, m0, 0, tcsm, bar, tmem, acc);
 
   if constexpr (MODE == Z_RESTORE) {
     if (valid) {
 #pragma unroll
-      for (int kz = 0; kz < N3; ++kz) a.Tout[(int64_t)kz * a.n12 + ij] = make_float2(acc[2 * kz], acc[2 * kz + 1]);
+      for (int j = 0; j < BN / G; ++j) {
+        const int n = grp * (BN / G) + j;                       // column in (even, odd) order
+        const int kz = (G == 2) ? (n < N3 / 2 ? 2 * n : 2 * (n - N3 / 2) + 1) : n;
+        if (kz < N3) a.Tout[(int64_t)kz * a.n12 + ij] = make_float2(acc[2 * j], acc[2 * j + 1]);
+      }
     }
-  } else {
+  } else if constexpr (G == 1) {
 #pragma unroll
     for (int dq = 0; dq < ND; ++dq) {
       if (dq < nd) {
@@ -367,6 +409,38 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z(ZArgs a, int nq) {
 #pragma unroll
           for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
         }
+      }
+    }
+  } else {
+    // even (grp 0) / odd (grp 1) half-length transforms
+    constexpr int H = N3 / 2;                                   // = Nz
+    float2* Wl = a.W + (int64_t)q0 * Nz * a.n12 + (valid ? ij : 0);
+    float2 f[H];
+#pragma unroll
+    for (int z = 0; z < H; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int z = 1; z < H; ++z) f[z] = cmul(f[z], grp ? twc<N3, false>(z) : make_float2(1.f, 0.f));
+    fft_reg<H, false, false>(f);
+#pragma unroll
+    for (int m = 0; m < H; ++m) f[m] = cmul(make_float2(acc[2 * m], acc[2 * m + 1]), f[m]);
+    fft_reg<H, true, false>(f);
+#pragma unroll
+    for (int z = 1; z < H; ++z) f[z] = cmul(f[z], grp ? twc<N3, true>(z) : make_float2(1.f, 0.f));
+    // y = y_even + y_odd: each group finishes half of the z outputs (operand smem is free now)
+    float2* xs = reinterpret_cast<float2*>(tcsm);               // [2][H/2][128]
+    constexpr int HH = H / 2;
+    // group g keeps z in [g HH, (g+1) HH) and hands the other half to the other group
+#pragma unroll
+    for (int j = 0; j < HH; ++j) {
+      const float2 give = grp ? f[j] : f[HH + j];            // selects between two registers
+      xs[(grp * HH + j) * 128 + row] = give;
+    }
+    __syncthreads();
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < HH; ++j) {
+        const float2 keep = grp ? f[HH + j] : f[j];
+        Wl[(int64_t)(grp * HH + j) * a.n12] = cadd(keep, xs[((1 - grp) * HH + j) * 128 + row]);
       }
     }
   }
