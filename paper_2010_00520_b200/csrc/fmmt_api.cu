@@ -310,7 +310,8 @@ void fmmt_op_destroy(fmmt_op* op) {
 // per-direction workspace bytes for batch sizing
 static int64_t per_dir_ws(const fmmt_op* op) {
   const int64_t n12 = op->n1 * op->n2, Nz = op->n3 / 2;
-  int64_t e = Nz * n12;   // W
+  int64_t e = 0;   // (W, the half-padded spectra, is allocated for all directions)
+  (void)Nz;
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D: e += op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
@@ -492,7 +493,7 @@ static fmmt_status build_plans(fmmt_op* op) {
   }
   const int64_t PB = op->PB;
   fmmt_status st;
-  if ((st = cmalloc(op, &op->W, PB * Nz * n12))) return st;
+  if ((st = cmalloc(op, &op->W, op->ndir * Nz * n12))) return st;   // all directions: one xy FFT launch each way
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D:
@@ -738,12 +739,12 @@ static fmmt_status launch_tc1_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a)
   return FMMT_OK;
 }
 
-static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout) {
+static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0) {
   fmmt_ctx* ctx = op->ctx;
   if (ctx->gemm_impl >= 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
     fill_zargs(op, a);
-    a.W = op->W + (int64_t)qoff * (op->n3 / 2) * a.n12;
+    a.W = op->W + (woff + (int64_t)qoff) * (op->n3 / 2) * a.n12;
     a.p0 = p0;
     a.G = a.G + (int64_t)qoff * a.g_stride;
     if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
@@ -770,7 +771,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
   ZArgs a;
   fill_zargs(op, a);
-  a.W = op->W + (int64_t)qoff * (op->n3 / 2) * a.n12;
+  a.W = op->W + (woff + (int64_t)qoff) * (op->n3 / 2) * a.n12;
   a.p0 = p0;
   a.G = a.G ? a.G + (int64_t)qoff * a.g_stride : nullptr;
   if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
@@ -797,14 +798,17 @@ static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64*
   const float scale = (float)(1.0 / ((double)op->n1 * (double)op->n2 * (double)op->n3));
   const float2* in = reinterpret_cast<const float2*>(sig_in);
   float2* out = reinterpret_cast<float2*>(sig_out);
+  // a1-a2: pruned x/y DFTs of all directions' planes in one launch (W holds every direction's
+  // half-padded spectrum); per L2-sized batch: restore chain + fused z-stage; a6: one launch back.
+  fmmt_status st;
+  if ((st = launch_xy(op, true, in, op->W, (int)(op->ndir * Nz), 1.f))) return st;
   for (const Batch& b : op->batches) {
-    fmmt_status st;
     if ((st = run_batch_prep(op, b))) return st;
-    if ((st = launch_xy(op, true, in + (int64_t)b.q0 * K, op->W, b.nq * Nz, 1.f))) return st;
     const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
-    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr))) return st;
-    if ((st = launch_xy(op, false, op->W, out + (int64_t)b.q0 * K, b.nq * Nz, scale))) return st;
+    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr, b.q0))) return st;
   }
+  if ((st = launch_xy(op, false, op->W, out, (int)(op->ndir * Nz), scale))) return st;
+  (void)K;
   return FMMT_OK;
 }
 
@@ -1351,7 +1355,8 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
       fmmt_op_destroy(op);
       return st;
     }
-    if ((st = pack_a(op, gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0), &op->E_pk))) {
+    if (ctx->pack_factors &&
+        (st = pack_a(op, gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0), &op->E_pk))) {
       fmmt_op_destroy(op);
       return st;
     }
@@ -1375,8 +1380,10 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
       return tst;
     }
     const int64_t n12 = n1 * n2;
-    fmmt_status pst = pack_a(op, gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0),
-                             &op->tbar1_pk);
+    fmmt_status pst = ctx->pack_factors
+                          ? pack_a(op, gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0),
+                                   &op->tbar1_pk)
+                          : FMMT_OK;
     if (pst) {
       fmmt_op_destroy(op);
       return pst;

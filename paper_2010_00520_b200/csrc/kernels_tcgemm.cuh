@@ -35,7 +35,8 @@ namespace fmmt {
 
 constexpr int TC_BM = 128;      // rows per tile (UMMA M)
 constexpr int TC_BK = 8;        // complex K per chunk (16 real = 2 UMMA K-steps)
-constexpr int TC_NS = 3;        // operand ring stages (MMAs of chunk k-1 overlap the conversion of chunk k)
+constexpr int TC_NS = 4;        // operand ring stages: copies run 2 chunks ahead, MMAs of chunk k-1 overlap
+                                // the conversion of chunk k
 constexpr int TC_PACK_FLOATS = 2 * TC_BM * 2 * TC_BK;   // one packed A tile: hi + lo, 128 x 16 real
 constexpr int TC_FC = 2;        // chunks per TMEM flush group (4 K-steps per accumulator chain; 8 fails the 1e-6 restore bar)
 
@@ -78,7 +79,12 @@ __device__ __forceinline__ void tc_flush(uint32_t tslot_addr, int c0, float (&ac
     tc::tmem_ld16(tslot_addr + c0 + c, vm);
     tc::tmem_ld16(tslot_addr + NR + c0 + c, vx);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[c + j] += vm[j] + vx[j];
+    for (int j = 0; j < 16; j += 2) {   // acc += (hi.hi + cross), two columns per FADD2
+      const float2 t = cadd(make_float2(acc[c + j], acc[c + j + 1]),
+                            cadd(make_float2(vm[j], vm[j + 1]), make_float2(vx[j], vx[j + 1])));
+      acc[c + j] = t.x;
+      acc[c + j + 1] = t.y;
+    }
   }
 }
 
@@ -172,44 +178,59 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     tc::cp_async_commit();
   };
 
-  // bar[0 .. TC_NS): MMA commit of the chunk in stage s; bar[TC_NS .. 2 TC_NS): packed-A copies.
-  // Chunk c uses stage c % TC_NS (phase (c / TC_NS) & 1 of its barriers) and TMEM slot
-  // (c / TC_FC) & 1.
+  // Barrier-free pipeline (no __syncthreads in the K loop).  Every thread converts exactly the
+  // shared-memory segments its own cp.async copied, fences them for the async proxy and arrives
+  // on full[s]; thread 0 waits for the 128 arrivals, issues the chunk's MMAs and commits them to
+  // mma[s]; a stage is refilled once mma[s] completed; TMEM slots are handed back through tfree.
+  //   bar[0, NS) mma commits   bar[NS, 2NS) packed-A bulk copies   bar[2NS, 3NS) full (128)
+  //   bar[3NS, 3NS+2) tfree (128), one per TMEM slot
+  // Chunk c: stage c % NS, phase (c / NS) & 1; flush group g = c / FC: slot g & 1, phase (g / 2) & 1.
+  static_assert(G == 1, "own-segment conversion mapping assumes one thread group");
+  uint64_t* mmab = bar;
+  uint64_t* abar = bar + TC_NS;
+  uint64_t* full = bar + 2 * TC_NS;
+  uint64_t* tfree = bar + 3 * TC_NS;
   int flushed = 0;                       // flush groups already drained into acc
   auto drain_complete = [&](int done) {  // chunks [0, done) have completed MMAs
-    for (; (flushed + 1) * TC_FC <= done; ++flushed)
+    for (; (flushed + 1) * TC_FC <= done; ++flushed) {
       tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tfree[flushed & 1]);
+    }
   };
-  issue(0);
+  constexpr int D = TC_NS - 2;           // copy prefetch distance (chunks)
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    if (c < nk) issue(c);
+    else tc::cp_async_commit();
+  }
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc % TC_NS;
+    const uint32_t ph = (kc / TC_NS) & 1;
     if (kc >= 2) {
-      // MMAs of chunk kc-2 (and earlier) complete: stage (kc+1) % NS is free, closed groups drain
-      tc::mbar_wait(&bar[(kc - 2) % TC_NS], ((kc - 2) / TC_NS) & 1);
+      // MMAs of chunk kc-2 (and earlier) complete: stage (kc+2) % NS is free, closed groups drain
+      tc::mbar_wait(&mmab[(kc - 2) % TC_NS], ((kc - 2) / TC_NS) & 1);
       tc::fence_after_sync();
       drain_complete(kc - 1);
     }
-    if (kc + 1 < nk) {
-      issue(kc + 1);
-      tc::cp_async_wait<1>();
-    } else {
-      tc::cp_async_wait<0>();
-    }
-    if (apack) tc::mbar_wait(&bar[TC_NS + s], (kc / TC_NS) & 1);   // packed A of chunk kc has landed
-    __syncthreads();                                 // chunk kc's A_hi (all threads' copies) is in place
+    if (kc + D < nk) issue(kc + D);
+    else tc::cp_async_commit();          // keep one group per iteration
+    tc::cp_async_wait<D>();              // this thread's copies of chunk kc have landed
+    if (apack) tc::mbar_wait(&abar[s], ph);
     uint8_t* st = tcsm + s * Cfg::STAGE;
     uint8_t* aHi = st;
     uint8_t* aLo = st + Cfg::A_BYTES;
     uint8_t* bP = st + 2 * Cfg::A_BYTES;
     const uint8_t* bRaw = bP + Cfg::BP_BYTES;
-    // ---- round A in place to A_hi = rna_tf32(x) and write A_lo = rna_tf32(x - A_hi) next to it
-    //      (same canonical offsets).  Round-to-nearest on both parts keeps |x - hi - lo| and the
-    //      dropped lo.lo product at 2^-22 |x| (truncated hi doubles both: measured restore errors
-    //      up to 1.02e-6 against the 1e-6 bar).
+    // ---- round this thread's A segments in place to A_hi = rna_tf32(x), A_lo = rna_tf32(x - A_hi)
+    //      next to them.  Round-to-nearest on both parts keeps |x - hi - lo| and the dropped lo.lo
+    //      product at 2^-22 |x| (a truncated hi doubles both: measured restore errors up to 1.02e-6
+    //      against the 1e-6 bar).
     if (!apack) {
 #pragma unroll
-      for (int i = 0; i < Cfg::A_BYTES / (16 * NT); ++i) {
-        const uint32_t off = (i * NT + tid) * 16;
+      for (int u = 0; u < BK / 2; ++u) {
+        const uint32_t off = a_kcontig ? ((lane & 7) + 8 * (u + 4 * wrow)) * 16 + (lane >> 3) * Cfg::LBO_A
+                                       : row * 16 + u * Cfg::LBO_A;
         const float4 a = *reinterpret_cast<const float4*>(aHi + off);
         float4 hi, lo;
         tc::split_tf32(a.x, hi.x, lo.x);
@@ -243,14 +264,16 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       *reinterpret_cast<float4*>(bP + off + NR * 16 + 16) = l1;
     }
     tc::fence_async_smem();
-    tc::fence_before_sync();
-    __syncthreads();
+    tc::mbar_arrive(&full[s]);
     if (tid == 0) {
+      tc::mbar_wait(&full[s], ph);                    // all 128 threads' operands of chunk kc are in place
+      const int g = kc / TC_FC;
+      const bool fresh = kc % TC_FC == 0;             // first chunk of a flush group
+      if (fresh && g >= 2) tc::mbar_wait(&tfree[g & 1], ((g >> 1) - 1) & 1);   // group g-2 drained
       tc::fence_after_sync();
       const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
       const uint32_t sb = sa_hi + 2 * Cfg::A_BYTES;
-      const uint32_t tm = tmem + ((kc / TC_FC) & 1) * 2 * NR, tx = tm + NR;
-      const bool fresh = kc % TC_FC == 0;              // first chunk of a flush group (slot freed at kc-1)
+      const uint32_t tm = tmem + (g & 1) * 2 * NR, tx = tm + NR;
 #pragma unroll
       for (int ks = 0; ks < Cfg::KR / 8; ++ks) {
         const uint64_t ah = tc::sdesc(sa_hi + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
@@ -259,11 +282,12 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
         tc::mma_tf32(tm, ah, bp, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
         tc::mma_tf32(tx, al, bp, IDESC_B, 1);                       // += lo.hi  (rows [0, NR) of B')
       }
-      tc::mma_commit(&bar[s]);
+      tc::mma_commit(&mmab[s]);
     }
   }
+  tc::cp_async_wait<0>();
   // drain the remaining flush groups (the last one possibly partial)
-  tc::mbar_wait(&bar[(nk - 1) % TC_NS], ((nk - 1) / TC_NS) & 1);
+  tc::mbar_wait(&mmab[(nk - 1) % TC_NS], ((nk - 1) / TC_NS) & 1);
   tc::fence_after_sync();
   drain_complete(nk);
   if (flushed * TC_FC < nk) tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
@@ -275,7 +299,9 @@ __device__ __forceinline__ uint32_t tc_setup(uint64_t* bar, uint32_t* tslot) {
   if ((threadIdx.x >> 5) == 0) tc::tmem_alloc<TMEM_COLS>(tslot);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < 2 * TC_NS; ++i) tc::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 2 * TC_NS; ++i) tc::mbar_init(&bar[i], 1);      // MMA commits, bulk copies
+#pragma unroll
+    for (int i = 2 * TC_NS; i < 3 * TC_NS + 2; ++i) tc::mbar_init(&bar[i], 128);   // full, tfree
     tc::fence_barrier_init();
   }
   tc::fence_before_sync();
@@ -296,7 +322,7 @@ __global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int BM = TC_BM, NRG = Cfg::NRG;
   extern __shared__ __align__(1024) uint8_t tcsm[];
-  __shared__ __align__(8) uint64_t bar[2 * TC_NS];
+  __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
   __shared__ uint32_t tslot;
 
   const GemmDesc d = descs[blockIdx.z];
@@ -353,7 +379,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
   static_assert(ND == 1 || MODE != Z_RESTORE, "restore hook is per direction");
   static_assert(G == 1 || (ND == 1 && BN == N3), "column groups split one direction's kz");
   extern __shared__ __align__(1024) uint8_t tcsm[];
-  __shared__ __align__(8) uint64_t bar[2 * TC_NS];
+  __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
   __shared__ uint32_t tslot;
 
   const int q0 = blockIdx.y * ND;
