@@ -286,6 +286,30 @@ def run_ours(args):
             for kname, v in kernel_work(info, fmt, op.ranks(), dn).items():
                 kwork[kname] = kwork.get(kname, 0.0) + v * PROF_STEPS
 
+        # two-component signatures: theta and phi share one restore per direction
+        sig2 = torch.from_numpy(np.ascontiguousarray(
+            signatures(signature_seed(args.config, 2), 2 * ndir, *N).reshape(ndir, 2, cfg.Nz, cfg.Ny, cfg.Nx)[d0:d0 + dn])).cuda()
+        sums2 = torch.empty((2, cfg.Nz, cfg.Ny, cfg.Nx), dtype=torch.complex64, device="cuda")
+        for _ in range(3):
+            for _, _, op in ops:
+                op.translate_sum_multi(sig2, None, wd, sums2, dn, 2, N)
+        ms2 = []
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _, _, op in ops:
+                op.translate_sum_multi(sig2, None, wd, sums2, dn, 2, N)
+            e1.record(stream)
+            e1.synchronize()
+            ms2.append(e0.elapsed_time(e1))
+        two_comp_ms = float(np.mean(ms2))
+        if world > 1:
+            tt = torch.tensor([two_comp_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            two_comp_ms = float(tt[0])
+        del sig2
+
         # end-to-end through the C ABI with host buffers (pinned), per step:
         # H2D of the signatures + weights, the matvec, D2H of the summed result
         sig_h = torch.from_numpy(signatures(signature_seed(args.config, 1), ndir, *N)[d0:d0 + dn]).pin_memory()
@@ -394,6 +418,10 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(len(ops) * (ndir * K * 8 + ndir * 4)),
                 "d2h_bytes_per_step": int(len(ops) * K * 8)},
         "dense_ms": round(dense_ms, 4),
+        "two_component": {"value": round(2 * total_units / (two_comp_ms * 1e-3) / 1e9, 3), "unit": "Gdir*pt/s",
+                          "ms_per_step": round(two_comp_ms, 4),
+                          "note": "theta+phi signatures [ndir][2][Nz][Ny][Nx], one restore per direction serves both "
+                                  "(SURVEY 8(f) NEXT #1); units count both components"},
         "per_format": per_format,
         "kernels": kernels,
         "setup_s": round(t_setup, 1),

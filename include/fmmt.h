@@ -227,6 +227,19 @@ fmmt_status fmmt_translate_sum(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* si
                                const float* w, fmmt_c64* sum_out,
                                int64_t ndir, int64_t Nx, int64_t Ny, int64_t Nz);
 
+/* Multi-component signatures (the aggregated far fields have a theta and
+ * a phi component, both translated by the same operator).  One restoration of
+ * T_p serves all ncomp components.
+ *   sig_in, sig_out: device complex64 [ndir][ncomp][Nz][Ny][Nx], ncomp in [1, 16].
+ *   fmmt_translate_sum_multi: sum_out [ncomp][Nz][Ny][Nx] (per-component direction
+ *   sum, allreduced over shards); sig_out may be NULL.
+ * ncomp = 1 is exactly fmmt_translate / fmmt_translate_sum.                  */
+fmmt_status fmmt_translate_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int64_t ndir, int64_t ncomp,
+                                 int64_t Nx, int64_t Ny, int64_t Nz);
+fmmt_status fmmt_translate_sum_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, const float* w,
+                                     fmmt_c64* sum_out, int64_t ndir, int64_t ncomp, int64_t Nx, int64_t Ny,
+                                     int64_t Nz);
+
 /* End-to-end variant on HOST buffers: copies sig_in (host, [ndir][Nz][Ny][Nx])
  * and w (host) to the device, runs fmmt_translate_sum, copies the summed
  * result to sum_out (host [Nz][Ny][Nx]) and synchronises the stream.

@@ -244,8 +244,10 @@ struct fmmt_op {
   float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
   std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
   int64_t pack_bytes = 0;
+  int64_t w_ncomp = 1;                         // signature components W is allocated for
   // workspace
   int64_t PB = 0;
+  int64_t sigtmp_elems = 0;
   float2 *W = nullptr, *H = nullptr, *Gw = nullptr, *Cw = nullptr, *Mw = nullptr, *Nw = nullptr,
          *Vw = nullptr, *sigtmp = nullptr, *partial = nullptr;
   int64_t ws_bytes = 0;
@@ -254,9 +256,10 @@ struct fmmt_op {
   GemmDesc* d_descs = nullptr;
   std::vector<Batch> batches;
   int nsplit = 1;
+  int64_t partial_elems = 0;
   // CUDA graphs of whole matvecs, keyed by the buffers they read / write
   struct GraphEntry {
-    const void* key[4];
+    const void* key[5];
     int calls = 0;
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;   // kernels inside the graph
@@ -493,7 +496,7 @@ static fmmt_status build_plans(fmmt_op* op) {
   }
   const int64_t PB = op->PB;
   fmmt_status st;
-  if ((st = cmalloc(op, &op->W, op->ndir * Nz * n12))) return st;   // all directions: one xy FFT launch each way
+  if ((st = cmalloc(op, &op->W, op->ndir * op->w_ncomp * Nz * n12))) return st;   // all directions (one xy launch each way)
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D:
@@ -739,12 +742,14 @@ static fmmt_status launch_tc1_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a)
   return FMMT_OK;
 }
 
-static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0) {
+static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0,
+                            int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
   if (ctx->gemm_impl >= 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
     fill_zargs(op, a);
-    a.W = op->W + (woff + (int64_t)qoff) * (op->n3 / 2) * a.n12;
+    a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
+    a.ncomp = ncomp;
     a.p0 = p0;
     a.G = a.G + (int64_t)qoff * a.g_stride;
     if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
@@ -771,7 +776,8 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
   ZArgs a;
   fill_zargs(op, a);
-  a.W = op->W + (woff + (int64_t)qoff) * (op->n3 / 2) * a.n12;
+  a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
+  a.ncomp = ncomp;
   a.p0 = p0;
   a.G = a.G ? a.G + (int64_t)qoff * a.g_stride : nullptr;
   if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
@@ -792,35 +798,54 @@ static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
   return FMMT_OK;
 }
 
-static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out) {
-  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
+// W (the half-padded spectra of every direction and component) sized for ncomp components.
+static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
+  if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
+  fmmt_ctx* ctx = op->ctx;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& g : op->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  op->graphs.clear();
+  const int64_t elems = op->ndir * (op->n3 / 2) * op->n1 * op->n2;
+  if (op->W) {
+    cudaFree(op->W);
+    op->ws_bytes -= op->w_ncomp * elems * 8;
+    op->W = nullptr;
+  }
+  op->w_ncomp = std::max<int64_t>(ncomp, op->w_ncomp);
+  return cmalloc(op, &op->W, op->w_ncomp * elems);
+}
+
+static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int ncomp = 1) {
   const int Nz = (int)(op->n3 / 2);
   const float scale = (float)(1.0 / ((double)op->n1 * (double)op->n2 * (double)op->n3));
   const float2* in = reinterpret_cast<const float2*>(sig_in);
   float2* out = reinterpret_cast<float2*>(sig_out);
-  // a1-a2: pruned x/y DFTs of all directions' planes in one launch (W holds every direction's
-  // half-padded spectrum); per L2-sized batch: restore chain + fused z-stage; a6: one launch back.
+  // a1-a2: pruned x/y DFTs of all directions' (and components') planes in one launch (W holds
+  // every half-padded spectrum, layout [p][comp][z]); per L2-sized batch: restore chain + fused
+  // z-stage (one restore of T_p serves all ncomp components); a6: one launch back.
   fmmt_status st;
-  if ((st = launch_xy(op, true, in, op->W, (int)(op->ndir * Nz), 1.f))) return st;
+  const int planes = (int)(op->ndir * ncomp * Nz);
+  if ((st = launch_xy(op, true, in, op->W, planes, 1.f))) return st;
   for (const Batch& b : op->batches) {
     if ((st = run_batch_prep(op, b))) return st;
     const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
-    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr, b.q0))) return st;
+    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr, b.q0, ncomp))) return st;
   }
-  if ((st = launch_xy(op, false, op->W, out, (int)(op->ndir * Nz), scale))) return st;
-  (void)K;
+  if ((st = launch_xy(op, false, op->W, out, planes, scale))) return st;
   return FMMT_OK;
 }
 
 static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void* out, int64_t ndir, int64_t Nx,
-                                        int64_t Ny, int64_t Nz) {
+                                        int64_t Ny, int64_t Nz, int64_t ncomp = 1) {
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
   CHECK_ARG(ctx, in && out, "null signature pointer");
   CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
   CHECK_SHAPE(ctx, 2 * Nx == op->n1 && 2 * Ny == op->n2 && 2 * Nz == op->n3, "grid %lldx%lldx%lld does not match op n=%lldx%lldx%lld",
               (long long)Nx, (long long)Ny, (long long)Nz, (long long)op->n1, (long long)op->n2, (long long)op->n3);
-  const int64_t bytes = ndir * Nx * Ny * Nz * 8;
+  CHECK_ARG(ctx, ncomp >= 1 && ncomp <= 16, "ncomp %lld not in [1, 16]", (long long)ncomp);
+  const int64_t bytes = ndir * ncomp * Nx * Ny * Nz * 8;
   const char* a = (const char*)in;
   const char* b = (const char*)out;
   CHECK_ARG(ctx, a + bytes <= b || b + bytes <= a, "sig_in and sig_out overlap");
@@ -843,7 +868,8 @@ static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void*
 // launches per matvec).  Direct launches when profiling (per-kernel events) or
 // on the legacy default stream (not capturable).
 template <class F>
-static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, const void* k2, const void* k3, F&& body) {
+static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, const void* k2, const void* k3, int64_t k4,
+                               F&& body) {
   fmmt_ctx* ctx = op->ctx;
   if (ctx->stream == nullptr || !ctx->use_graphs) return body();
   if (ctx->profiling) {
@@ -868,7 +894,7 @@ static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, cons
   }
   fmmt_op::GraphEntry* ge = nullptr;
   for (auto& g : op->graphs)
-    if (g.key[0] == k0 && g.key[1] == k1 && g.key[2] == k2 && g.key[3] == k3) ge = &g;
+    if (g.key[0] == k0 && g.key[1] == k1 && g.key[2] == k2 && g.key[3] == k3 && g.key[4] == (const void*)k4) ge = &g;
   if (ge && ge->exec) {
     FMMT_CUDA(ctx, cudaGraphLaunch(ge->exec, ctx->stream));
     ctx->launches += ge->launches;
@@ -876,7 +902,7 @@ static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, cons
   }
   if (!ge) {   // first call: run directly (allocates lazily sized workspaces), remember the key
     fmmt_op::GraphEntry e;
-    e.key[0] = k0; e.key[1] = k1; e.key[2] = k2; e.key[3] = k3;
+    e.key[0] = k0; e.key[1] = k1; e.key[2] = k2; e.key[3] = k3; e.key[4] = (const void*)k4;
     e.calls = 1;
     op->graphs.push_back(e);
     return body();
@@ -1125,19 +1151,31 @@ fmmt_status fmmt_translate(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_ou
   fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
   if (st) return st;
   cudaSetDevice(op->ctx->device);
-  return run_graphed(op, sig_in, sig_out, nullptr, nullptr, [&] { return translate_impl(op, sig_in, sig_out); });
+  if ((st = ensure_w(op, 1))) return st;
+  return run_graphed(op, sig_in, sig_out, nullptr, nullptr, 1, [&] { return translate_impl(op, sig_in, sig_out, 1); });
 }
 
-static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float* w, float2* sum_out) {
+fmmt_status fmmt_translate_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int64_t ndir, int64_t ncomp,
+                                 int64_t Nx, int64_t Ny, int64_t Nz) {
+  fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz, ncomp);
+  if (st) return st;
+  cudaSetDevice(op->ctx->device);
+  if ((st = ensure_w(op, ncomp))) return st;
+  return run_graphed(op, sig_in, sig_out, nullptr, nullptr, ncomp,
+                     [&] { return translate_impl(op, sig_in, sig_out, (int)ncomp); });
+}
+
+static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float* w, float2* sum_out, int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
-  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
+  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2) * ncomp;   // [comp][Nz][Ny][Nx] per direction
   const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(op->ndir, std::max<int64_t>(1, (148 * 8 * 128) / std::max<int64_t>(K, 1))));
-  if (!op->partial || op->nsplit < nsplit) {
+  if (!op->partial || op->nsplit < nsplit || op->partial_elems < (int64_t)nsplit * K) {
     if (op->partial) cudaFree(op->partial);
     op->partial = nullptr;
     fmmt_status st = cmalloc(op, &op->partial, (int64_t)nsplit * K);
     if (st) return st;
     op->nsplit = nsplit;
+    op->partial_elems = (int64_t)nsplit * K;
   }
   {
     ProfScope ps(ctx, "dirsum_partial");
@@ -1157,28 +1195,38 @@ static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float
   return FMMT_OK;
 }
 
-fmmt_status fmmt_translate_sum(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, const float* w, fmmt_c64* sum_out,
-                               int64_t ndir, int64_t Nx, int64_t Ny, int64_t Nz) {
+fmmt_status fmmt_translate_sum_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, const float* w,
+                                     fmmt_c64* sum_out, int64_t ndir, int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz) {
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
   CHECK_ARG(ctx, w && sum_out, "null weight or sum pointer");
+  CHECK_ARG(ctx, ncomp >= 1 && ncomp <= 16, "ncomp %lld not in [1, 16]", (long long)ncomp);
   cudaSetDevice(ctx->device);
-  const int64_t K = Nx * Ny * Nz;
   if (!sig_out) {
-    if (!op->sigtmp) {
-      fmmt_status st = cmalloc(op, &op->sigtmp, op->ndir * (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2));
+    const int64_t need = op->ndir * ncomp * (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
+    if (!op->sigtmp || op->sigtmp_elems < need) {
+      if (op->sigtmp) cudaFree(op->sigtmp);
+      op->sigtmp = nullptr;
+      fmmt_status st = cmalloc(op, &op->sigtmp, need);
       if (st) return st;
+      op->sigtmp_elems = need;
     }
     sig_out = reinterpret_cast<fmmt_c64*>(op->sigtmp);
   }
-  fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz);
+  fmmt_status st = check_translate_args(op, sig_in, sig_out, ndir, Nx, Ny, Nz, ncomp);
   if (st) return st;
-  (void)K;
-  return run_graphed(op, sig_in, sig_out, w, sum_out, [&] {
-    fmmt_status s2 = translate_impl(op, sig_in, sig_out);
+  if ((st = ensure_w(op, ncomp))) return st;
+  return run_graphed(op, sig_in, sig_out, w, sum_out, ncomp, [&] {
+    fmmt_status s2 = translate_impl(op, sig_in, sig_out, (int)ncomp);
     if (s2) return s2;
-    return dirsum_and_reduce(op, reinterpret_cast<const float2*>(sig_out), w, reinterpret_cast<float2*>(sum_out));
+    return dirsum_and_reduce(op, reinterpret_cast<const float2*>(sig_out), w, reinterpret_cast<float2*>(sum_out),
+                             (int)ncomp);
   });
+}
+
+fmmt_status fmmt_translate_sum(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, const float* w, fmmt_c64* sum_out,
+                               int64_t ndir, int64_t Nx, int64_t Ny, int64_t Nz) {
+  return fmmt_translate_sum_multi(op, sig_in, sig_out, w, sum_out, ndir, 1, Nx, Ny, Nz);
 }
 
 fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, const float* w_host, fmmt_c64* sum_out_host,

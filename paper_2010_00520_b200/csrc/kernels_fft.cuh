@@ -302,8 +302,9 @@ k_inv_xy(const float2* __restrict__ W, float2* __restrict__ sig_out, int nplanes
 enum ZMode { Z_DENSE = 0, Z_LOWRANK = 1, Z_RESTORE = 2 };
 
 struct ZArgs {
-  float2* W;                 // batch workspace [q][Nz][n12]
+  float2* W;                 // half-padded spectra [q][comp][Nz][n12] (from the batch's first direction)
   int64_t n12;
+  int ncomp;                 // signature components sharing one restored T_p (theta, phi)
   int p0;                    // op-local index of the batch's first direction
   // low-rank factors: T_p[ij, k] = sum_c G_p[c][ij] * V_p(c, k)
   const float2* G;           // base
@@ -388,50 +389,53 @@ k_conv_z(ZArgs a) {
     return;
   }
 
-  // forward z-DFT of this line of the half-padded spectrum (z < Nz nonzero)
-  float2* Wl = a.W + (int64_t)q * Nz * a.n12 + (valid ? ij : 0);
-  float2 f[M];
-  if constexpr (S == 1) {
+  // per signature component: forward z-DFT of this line of the half-padded spectrum
+  // (z < Nz nonzero), Hadamard with the restored line t, inverse z-DFT truncated
+  for (int cc = 0; cc < a.ncomp; ++cc) {
+    float2* Wl = a.W + ((int64_t)q * a.ncomp + cc) * Nz * a.n12 + (valid ? ij : 0);
+    float2 f[M];
+    if constexpr (S == 1) {
 #pragma unroll
-    for (int z = 0; z < Nz; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
-    fft_reg<N3, false, true>(f);
-  } else {
-    // X[2m + h] = DFT_M( a[z0] * W_N3^{h z0} )[m], z0 < M = Nz
+      for (int z = 0; z < Nz; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
+      fft_reg<N3, false, true>(f);
+    } else {
+      // X[2m + h] = DFT_M( a[z0] * W_N3^{h z0} )[m], z0 < M = Nz
 #pragma unroll
-    for (int z = 0; z < M; ++z) {
-      float2 v = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
-      f[z] = (h && z) ? cmul(v, twc<N3, false>(z)) : v;
+      for (int z = 0; z < M; ++z) {
+        float2 v = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
+        f[z] = (h && z) ? cmul(v, twc<N3, false>(z)) : v;
+      }
+      fft_reg<M, false, false>(f);
     }
-    fft_reg<M, false, false>(f);
-  }
-  // Hadamard (a5): Y = T (.) A^
+    // Hadamard (a5): Y = T (.) A^
 #pragma unroll
-  for (int m = 0; m < M; ++m) f[m] = cmul(t[m], f[m]);
-  // inverse z-DFT, truncated to z < Nz
-  fft_reg<M, true, false>(f);
-  if constexpr (S == 1) {
-    if (valid) {
+    for (int m = 0; m < M; ++m) f[m] = cmul(t[m], f[m]);
+    // inverse z-DFT, truncated to z < Nz
+    fft_reg<M, true, false>(f);
+    if constexpr (S == 1) {
+      if (valid) {
 #pragma unroll
-      for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
-    }
-  } else {
-    // y[z] = c_0[z] + W_N3^{-z} c_1[z], z < M; thread h keeps z in [h*M/2, (h+1)*M/2)
+        for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
+      }
+    } else {
+      // y[z] = c_0[z] + W_N3^{-z} c_1[z], z < M; thread h keeps z in [h*M/2, (h+1)*M/2)
 #pragma unroll
-    for (int z = 1; z < M; ++z)
-      if (h) f[z] = cmul(f[z], twc<N3, true>(z));
-    float2 out[M / 2];
+      for (int z = 1; z < M; ++z)
+        if (h) f[z] = cmul(f[z], twc<N3, true>(z));
+      float2 out[M / 2];
 #pragma unroll
-    for (int j = 0; j < M / 2; ++j) {
-      float2 send = h ? f[j] : f[M / 2 + j];
-      float2 mine = h ? f[M / 2 + j] : f[j];
-      float2 recv;
-      recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-      recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-      out[j] = cadd(mine, recv);
-    }
-    if (valid) {
+      for (int j = 0; j < M / 2; ++j) {
+        float2 send = h ? f[j] : f[M / 2 + j];
+        float2 mine = h ? f[M / 2 + j] : f[j];
+        float2 recv;
+        recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+        recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+        out[j] = cadd(mine, recv);
+      }
+      if (valid) {
 #pragma unroll
-      for (int j = 0; j < M / 2; ++j) Wl[(int64_t)(h * (M / 2) + j) * a.n12] = out[j];
+        for (int j = 0; j < M / 2; ++j) Wl[(int64_t)(h * (M / 2) + j) * a.n12] = out[j];
+      }
     }
   }
 }

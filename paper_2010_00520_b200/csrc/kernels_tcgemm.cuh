@@ -92,11 +92,13 @@ __device__ __forceinline__ void tc_flush(uint32_t tslot_addr, int c0, float (&ac
 // the tile, re/im interleaved) = A[m0:m0+128, :] . B[:, n0:n0+BN] over all of K.
 // Called by all 128 G threads.  bar[0..1]: MMA commits per stage; bar[2..3]:
 // packed-A bulk copies per stage.
+// cb: this call's first global chunk number (a multiple of TC_FC; 0 for the first call of a CTA):
+// ring stages, barrier phases and TMEM flush groups continue across calls.  Returns the next cb.
 template <int BN, int G>
-__device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
-                                            const float2* __restrict__ B, int m0, int n0, uint8_t* tcsm,
-                                            uint64_t* bar, uint32_t tmem,
-                                            float (&acc)[TcGemmCfg<BN, G>::NRG]) {
+__device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
+                                           const float2* __restrict__ B, int m0, int n0, uint8_t* tcsm,
+                                           uint64_t* bar, uint32_t tmem,
+                                           float (&acc)[TcGemmCfg<BN, G>::NRG], int cb = 0) {
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int BM = TC_BM, BK = TC_BK, NR = Cfg::NR, NRG = Cfg::NRG, NT = Cfg::NT;
   constexpr int BITEMS = Cfg::BITEMS;
@@ -127,11 +129,12 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
   auto issue = [&](int c) {
     const int k0 = c * BK;
-    const uint32_t st = sbase + (c % TC_NS) * Cfg::STAGE;
+    const int cs = (cb + c) % TC_NS;
+    const uint32_t st = sbase + cs * Cfg::STAGE;
     if (apack) {
       if (tid == 0) {
-        tc::mbar_expect_tx(&bar[TC_NS + (c % TC_NS)], 2 * Cfg::A_BYTES);
-        tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[TC_NS + (c % TC_NS)]);
+        tc::mbar_expect_tx(&bar[TC_NS + cs], 2 * Cfg::A_BYTES);
+        tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[TC_NS + cs]);
       }
     } else if (!a_kcontig) {
       // row-per-thread: group g copies K elements [g BK/G, (g+1) BK/G) of its row
@@ -190,9 +193,9 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   uint64_t* abar = bar + TC_NS;
   uint64_t* full = bar + 2 * TC_NS;
   uint64_t* tfree = bar + 3 * TC_NS;
-  int flushed = 0;                       // flush groups already drained into acc
-  auto drain_complete = [&](int done) {  // chunks [0, done) have completed MMAs
-    for (; (flushed + 1) * TC_FC <= done; ++flushed) {
+  int flushed = cb / TC_FC;              // flush groups (global numbering) already drained into acc
+  auto drain_complete = [&](int done) {  // this call's chunks [0, done) have completed MMAs
+    for (; (flushed + 1) * TC_FC <= cb + done; ++flushed) {
       tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
       tc::fence_before_sync();
       tc::mbar_arrive(&tfree[flushed & 1]);
@@ -205,11 +208,13 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     else tc::cp_async_commit();
   }
   for (int kc = 0; kc < nk; ++kc) {
-    const int s = kc % TC_NS;
-    const uint32_t ph = (kc / TC_NS) & 1;
+    const int gc = cb + kc;                // global chunk number
+    const int s = gc % TC_NS;
+    const uint32_t ph = (gc / TC_NS) & 1;
     if (kc >= 2) {
       // MMAs of chunk kc-2 (and earlier) complete: stage (kc+2) % NS is free, closed groups drain
-      tc::mbar_wait(&mmab[(kc - 2) % TC_NS], ((kc - 2) / TC_NS) & 1);
+      // (for kc < 2 the stages were last used by a previous call, whose MMAs all completed)
+      tc::mbar_wait(&mmab[(gc - 2) % TC_NS], ((gc - 2) / TC_NS) & 1);
       tc::fence_after_sync();
       drain_complete(kc - 1);
     }
@@ -267,8 +272,8 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     tc::mbar_arrive(&full[s]);
     if (tid == 0) {
       tc::mbar_wait(&full[s], ph);                    // all 128 threads' operands of chunk kc are in place
-      const int g = kc / TC_FC;
-      const bool fresh = kc % TC_FC == 0;             // first chunk of a flush group
+      const int g = gc / TC_FC;
+      const bool fresh = gc % TC_FC == 0;             // first chunk of a flush group
       if (fresh && g >= 2) tc::mbar_wait(&tfree[g & 1], ((g >> 1) - 1) & 1);   // group g-2 drained
       tc::fence_after_sync();
       const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
@@ -287,10 +292,16 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   }
   tc::cp_async_wait<0>();
   // drain the remaining flush groups (the last one possibly partial)
-  tc::mbar_wait(&mmab[(nk - 1) % TC_NS], ((nk - 1) / TC_NS) & 1);
+  tc::mbar_wait(&mmab[(cb + nk - 1) % TC_NS], ((cb + nk - 1) / TC_NS) & 1);
   tc::fence_after_sync();
   drain_complete(nk);
-  if (flushed * TC_FC < nk) tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+  if (flushed * TC_FC < cb + nk) {
+    tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+    tc::fence_before_sync();
+    tc::mbar_arrive(&tfree[flushed & 1]);            // (keeps tfree phases aligned for a next call)
+    ++flushed;
+  }
+  return flushed * TC_FC;
 }
 
 // TMEM allocation + stage barriers (all threads call; warp 0 allocates).
@@ -363,11 +374,7 @@ __global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict
 // direction, the pruned forward z-DFT of the half-padded spectrum W, the
 // Hadamard product with T_p (a5) and the inverse z-DFT truncated to z < Nz
 // (a6), in registers.  T_p never leaves the SM.
-//   G = 2 (n3 = 16, 32): the two thread groups take the even and the odd kz
-//   (B's columns are ordered even kz first): with x the Nz nonzero inputs,
-//     A^[2m]   = DFT_{n3/2}(x)[m],            A^[2m+1] = DFT_{n3/2}(x W_n3^z)[m],
-//     y[z]     = IDFT_{n3/2}(T_even A^_even)[z] + W_n3^{-z} IDFT_{n3/2}(T_odd A^_odd)[z],
-//   and the two halves of y are added through shared memory.
+//   The ncomp signature components of a direction share the restored line.
 //   ND > 1 only when G is shared by all directions (TT-4D: G = T1 of Fig. 4(b))
 //   and V_q is laid out [q][kz][c] (one tile's B = ND directions side by side).
 template <int N3, int MODE, int ND, int G>
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int Nz = N3 / 2;
   static_assert(ND == 1 || MODE != Z_RESTORE, "restore hook is per direction");
-  static_assert(G == 1 || (ND == 1 && BN == N3), "column groups split one direction's kz");
+  static_assert(G == 1, "one thread group (thread = line ij)");
   extern __shared__ __align__(1024) uint8_t tcsm[];
   __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
   __shared__ uint32_t tslot;
@@ -418,11 +425,12 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
         if (kz < N3) a.Tout[(int64_t)kz * a.n12 + ij] = make_float2(acc[2 * j], acc[2 * j + 1]);
       }
     }
-  } else if constexpr (G == 1) {
+  } else {
 #pragma unroll
     for (int dq = 0; dq < ND; ++dq) {
-      if (dq < nd) {
-        float2* Wl = a.W + (int64_t)(q0 + dq) * Nz * a.n12 + (valid ? ij : 0);
+      if (dq >= nd) continue;
+      for (int cc = 0; cc < a.ncomp; ++cc) {   // signature components share the restored line
+        float2* Wl = a.W + ((int64_t)(q0 + dq) * a.ncomp + cc) * Nz * a.n12 + (valid ? ij : 0);
         float2 f[N3];
 #pragma unroll
         for (int z = 0; z < Nz; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
@@ -435,38 +443,6 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
 #pragma unroll
           for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
         }
-      }
-    }
-  } else {
-    // even (grp 0) / odd (grp 1) half-length transforms
-    constexpr int H = N3 / 2;                                   // = Nz
-    float2* Wl = a.W + (int64_t)q0 * Nz * a.n12 + (valid ? ij : 0);
-    float2 f[H];
-#pragma unroll
-    for (int z = 0; z < H; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
-#pragma unroll
-    for (int z = 1; z < H; ++z) f[z] = cmul(f[z], grp ? twc<N3, false>(z) : make_float2(1.f, 0.f));
-    fft_reg<H, false, false>(f);
-#pragma unroll
-    for (int m = 0; m < H; ++m) f[m] = cmul(make_float2(acc[2 * m], acc[2 * m + 1]), f[m]);
-    fft_reg<H, true, false>(f);
-#pragma unroll
-    for (int z = 1; z < H; ++z) f[z] = cmul(f[z], grp ? twc<N3, true>(z) : make_float2(1.f, 0.f));
-    // y = y_even + y_odd: each group finishes half of the z outputs (operand smem is free now)
-    float2* xs = reinterpret_cast<float2*>(tcsm);               // [2][H/2][128]
-    constexpr int HH = H / 2;
-    // group g keeps z in [g HH, (g+1) HH) and hands the other half to the other group
-#pragma unroll
-    for (int j = 0; j < HH; ++j) {
-      const float2 give = grp ? f[j] : f[HH + j];            // selects between two registers
-      xs[(grp * HH + j) * 128 + row] = give;
-    }
-    __syncthreads();
-    if (valid) {
-#pragma unroll
-      for (int j = 0; j < HH; ++j) {
-        const float2 keep = grp ? f[HH + j] : f[j];
-        Wl[(int64_t)(grp * HH + j) * a.n12] = cadd(keep, xs[((1 - grp) * HH + j) * 128 + row]);
       }
     }
   }

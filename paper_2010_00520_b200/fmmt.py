@@ -76,6 +76,8 @@ fmmt_translate = _sig("fmmt_translate", C.c_int, vp, vp, vp, i64, i64, i64, i64)
 fmmt_translate_sum = _sig("fmmt_translate_sum", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64)
 fmmt_translate_sum_host = _sig("fmmt_translate_sum_host", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64)
 fmmt_restore = _sig("fmmt_restore", C.c_int, vp, i64, vp)
+fmmt_translate_multi = _sig("fmmt_translate_multi", C.c_int, vp, vp, vp, i64, i64, i64, i64, i64)
+fmmt_translate_sum_multi = _sig("fmmt_translate_sum_multi", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64)
 fmmt_set_gemm_impl = _sig("fmmt_set_gemm_impl", C.c_int, vp, C.c_int)
 fmmt_test_cgemm = _sig("fmmt_test_cgemm", C.c_int, vp, C.c_int, i64, i64, i64, C.c_int, C.c_int, vp, i64, vp, i64, vp, i64)
 
@@ -85,6 +87,7 @@ EXPORTED = [
     "fmmt_launch_count", "fmmt_multipole_count", "fmmt_direction_grid", "fmmt_build_operator", "fmmt_compress",
     "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_set_batch", "fmmt_translate",
     "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
+    "fmmt_translate_multi", "fmmt_translate_sum_multi",
 ]
 
 
@@ -265,6 +268,14 @@ class Op:
     def translate_sum_host(self, sig_in_host, w_host, sum_out_host, ndir, N):
         _check(fmmt_translate_sum_host(self.h, _ptr(sig_in_host), _ptr(w_host), _ptr(sum_out_host), ndir,
                                        N[0], N[1], N[2]), self.ctx.h, "fmmt_translate_sum_host")
+
+    def translate_multi(self, sig_in, sig_out, ndir, ncomp, N):
+        _check(fmmt_translate_multi(self.h, _ptr(sig_in), _ptr(sig_out), ndir, ncomp, N[0], N[1], N[2]), self.ctx.h,
+               "fmmt_translate_multi")
+
+    def translate_sum_multi(self, sig_in, sig_out, w, sum_out, ndir, ncomp, N):
+        _check(fmmt_translate_sum_multi(self.h, _ptr(sig_in), _ptr(sig_out), _ptr(w), _ptr(sum_out), ndir, ncomp,
+                                        N[0], N[1], N[2]), self.ctx.h, "fmmt_translate_sum_multi")
 
     def restore(self, p: int, out):
         _check(fmmt_restore(self.h, p, _ptr(out)), self.ctx.h, "fmmt_restore")
