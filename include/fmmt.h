@@ -140,6 +140,14 @@ fmmt_status fmmt_build_operator(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t N
                                 double edge, double k, int64_t L,
                                 const double* khat, int64_t ndir, fmmt_c128* T);
 
+/* Lossy medium (Table IV): the same operator
+ * with a complex wavenumber k = k_re + j k_im, k_im <= 0 (e^{+j omega t}:
+ * eps_r = eps' - j eps'').  h_l^(2)(kR) by the upward recurrence from the closed
+ * forms h_0, h_1 (FP64, complex).  Choose L from |k| (fmmt_multipole_count).
+ * k_im = 0 is exactly fmmt_build_operator.  FMMT_E_ARG if k_im > 0.         */
+fmmt_status fmmt_build_operator_lossy(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t Nz, double edge, double k_re,
+                                      double k_im, int64_t L, const double* khat, int64_t ndir, fmmt_c128* T);
+
 /* ------------------------------------------------------- setup: compression */
 
 /* Compress the FFT'ed operator (Alg. 1 / 2 / 3) to relative

@@ -92,9 +92,22 @@ def offset_grid(Nx: int, Ny: int, Nz: int):
 
 def sph_hankel2(l: int, z):
     """Spherical Hankel function of the second kind h_l^(2)(z) = j_l(z) - i y_l(z)
-    (P:77), from SciPy's spherical Bessel functions (library primitive).
-    e^{+j omega t} convention: h_0^(2)(z) = j e^{-jz} / z."""
-    return special.spherical_jn(l, z) - 1j * special.spherical_yn(l, z)
+    (P:77).  e^{+j omega t} convention: h_0^(2)(z) = j e^{-jz} / z.
+
+    Real z: SciPy's spherical Bessel functions (library primitive).
+    Complex z (lossy media): the textbook terminating series
+        h_l^(2)(z) = j^{l+1} e^{-jz}/z  sum_{k=0}^{l} (l+k)! / (k! (l-k)!) (-j / (2z))^k,
+    which stays accurate when |Im z| is large (j_l and y_l then grow like
+    e^{|Im z|} and their difference h^(2) cancels catastrophically)."""
+    z = np.asarray(z)
+    if not np.iscomplexobj(z) or not np.any(np.imag(z) != 0):
+        return special.spherical_jn(l, np.real(z) if not np.iscomplexobj(z) else z) - 1j * special.spherical_yn(
+            l, np.real(z) if not np.iscomplexobj(z) else z)
+    acc = np.zeros(z.shape, dtype=np.complex128)
+    for k in range(l + 1):
+        coef = math.factorial(l + k) / (math.factorial(k) * math.factorial(l - k))
+        acc = acc + coef * (-1j / (2.0 * z)) ** k
+    return (1j ** (l + 1)) * np.exp(-1j * z) / z * acc
 
 
 def legendre(l: int, x):
@@ -102,13 +115,23 @@ def legendre(l: int, x):
     return special.eval_legendre(l, x)
 
 
+def medium_wavenumber(eps_r: complex, k0: float = 2.0 * math.pi) -> complex:
+    """k = k0 sqrt(eps_r) of a (lossy) medium, e^{+j omega t} convention: eps_r = eps' - j eps''
+    gives Im k <= 0, so h_l^(2)(kR) ~ e^{-jkR} decays with R (Table IV)."""
+    k = k0 * np.sqrt(complex(eps_r))
+    return complex(k.real, -abs(k.imag))
+
+
 class OperatorGrid:
     """Direction-independent part of eq. (7) on the circulant grid:
-    R = edge*|u|, R_hat, far mask, and h_l^(2)(kR) for l = 0..L."""
+    R = edge*|u|, R_hat, far mask, and h_l^(2)(kR) for l = 0..L.
+    k may be complex (lossy medium); L is then chosen from |k|."""
 
     def __init__(self, Nx, Ny, Nz, edge, k, L):
         self.Nx, self.Ny, self.Nz = int(Nx), int(Ny), int(Nz)
-        self.edge, self.k, self.L = float(edge), float(k), int(L)
+        self.edge, self.L = float(edge), int(L)
+        kc = complex(k)
+        self.k = kc.real if kc.imag == 0 else kc
         UX, UY, UZ, far = offset_grid(self.Nx, self.Ny, self.Nz)
         self.shape = far.shape
         self.far = far

@@ -220,11 +220,75 @@ __global__ void k_spatial_operator(double2* __restrict__ out, int n1, int n2, in
   out[(int64_t)p * n + idx] = res;
 }
 
-extern "C" fmmt_status fmmt_build_operator(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t Nz, double edge, double k,
-                                           int64_t L, const double* khat, int64_t ndir, fmmt_c128* T) {
+// Lossy medium (complex k): h_l^(2)(z) for complex z = kR by the upward
+// recurrence h_{l+1} = (2l+1)/z h_l - h_{l-1} from h_0 = j e^{-jz}/z, h_1 = e^{-jz}(j - z)/z^2
+// (h^(2) is the dominant solution, so the upward recurrence is stable).
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  const double den = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+}
+
+__global__ void k_spatial_operator_c(double2* __restrict__ out, int n1, int n2, int n3, double edge, double kr,
+                                     double ki, int L, const double* __restrict__ khat, int nd) {
+  const int64_t n = (int64_t)n1 * n2 * n3;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
+  if (idx >= n || p >= nd) return;
+  const int i1 = (int)(idx % n1), i2 = (int)((idx / n1) % n2), i3 = (int)(idx / ((int64_t)n1 * n2));
+  const int N1 = n1 / 2, N2 = n2 / 2, N3 = n3 / 2;
+  double2 res = make_double2(0.0, 0.0);
+  const bool onplane = (i1 == N1) || (i2 == N2) || (i3 == N3);
+  const int ux = i1 < N1 ? i1 : i1 - n1;
+  const int uy = i2 < N2 ? i2 : i2 - n2;
+  const int uz = i3 < N3 ? i3 : i3 - n3;
+  const int u2 = ux * ux + uy * uy + uz * uz;
+  if (!onplane && u2 > 12) {   // far iff |u|^2 > 12 (kappa = 4)
+    const double un = sqrt((double)u2);
+    const double R = edge * un;
+    const double c = (ux * khat[3 * p] + uy * khat[3 * p + 1] + uz * khat[3 * p + 2]) / un;
+    const double2 z = make_double2(kr * R, ki * R);
+    // e^{-jz} = e^{Im z} (cos Re z - j sin Re z)
+    double sr, cr;
+    sincos(z.x, &sr, &cr);
+    const double ea = exp(z.y);
+    const double2 emj = make_double2(ea * cr, -ea * sr);
+    const double2 h0 = zdiv(make_double2(-emj.y, emj.x), z);                        // j e^{-jz} / z
+    const double2 z2 = fmmt::zmul(z, z);
+    const double2 h1 = zdiv(fmmt::zmul(emj, make_double2(-z.x, 1.0 - z.y)), z2);         // e^{-jz} (j - z) / z^2
+    double2 hm1 = h0, hc = h1;
+    double Pm1 = 1.0, P0 = c;
+    for (int l = 0; l <= L; ++l) {
+      double2 hl;
+      double Pl;
+      if (l == 0) { hl = h0; Pl = 1.0; }
+      else if (l == 1) { hl = h1; Pl = c; }
+      else {
+        const double2 t = zdiv(make_double2((2 * l - 1) * hc.x, (2 * l - 1) * hc.y), z);
+        const double2 hn = make_double2(t.x - hm1.x, t.y - hm1.y);
+        hm1 = hc; hc = hn; hl = hn;
+        const double Pn = ((2 * l - 1) * c * P0 - (l - 1) * Pm1) / l;
+        Pm1 = P0; P0 = Pn; Pl = Pn;
+      }
+      const double f = (2 * l + 1) * Pl;
+      double tr, ti;
+      switch (l & 3) {                  // (-j)^l h_l
+        case 0: tr = hl.x; ti = hl.y; break;
+        case 1: tr = hl.y; ti = -hl.x; break;
+        case 2: tr = -hl.x; ti = -hl.y; break;
+        default: tr = -hl.y; ti = hl.x; break;
+      }
+      res.x += f * tr;
+      res.y += f * ti;
+    }
+  }
+  out[(int64_t)p * n + idx] = res;
+}
+
+static fmmt_status build_operator_impl(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t Nz, double edge, double k,
+                                       double k_im, int64_t L, const double* khat, int64_t ndir, fmmt_c128* T) {
   if (!ctx) return FMMT_E_ARG;
   if (!khat || !T) return set_err(ctx, FMMT_E_ARG, "null pointer");
-  if (Nx < 1 || Ny < 1 || Nz < 1 || ndir < 1 || L < 0 || L > LMAX - 1 || !(edge > 0) || !(k > 0))
+  if (Nx < 1 || Ny < 1 || Nz < 1 || ndir < 1 || L < 0 || L > LMAX - 1 || !(edge > 0) || !(k > 0) || k_im > 0)
     return set_err(ctx, FMMT_E_ARG, "bad operator parameters");
   cudaSetDevice(ctx->device);
   const int n1 = (int)(2 * Nx), n2 = (int)(2 * Ny), n3 = (int)(2 * Nz);
@@ -236,8 +300,12 @@ extern "C" fmmt_status fmmt_build_operator(fmmt_ctx* ctx, int64_t Nx, int64_t Ny
   for (int64_t p0 = 0; p0 < ndir; p0 += chunk) {
     const int nd = (int)std::min<int64_t>(chunk, ndir - p0);
     dim3 grid((unsigned)((n + 127) / 128), (unsigned)nd);
-    k_spatial_operator<<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<double2*>(T) + p0 * n, n1, n2, n3, edge, k, (int)L,
-                                                      dk + 3 * p0, nd);
+    if (k_im == 0.0)
+      k_spatial_operator<<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<double2*>(T) + p0 * n, n1, n2, n3, edge, k,
+                                                        (int)L, dk + 3 * p0, nd);
+    else
+      k_spatial_operator_c<<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<double2*>(T) + p0 * n, n1, n2, n3, edge, k,
+                                                          k_im, (int)L, dk + 3 * p0, nd);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
   // T = F(T~): unnormalised forward 3D DFT, batched over directions
@@ -272,6 +340,17 @@ extern "C" fmmt_status fmmt_build_operator(fmmt_ctx* ctx, int64_t Nx, int64_t Ny
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   cudaFree(dk);
   return FMMT_OK;
+}
+
+extern "C" fmmt_status fmmt_build_operator(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t Nz, double edge, double k,
+                                           int64_t L, const double* khat, int64_t ndir, fmmt_c128* T) {
+  return build_operator_impl(ctx, Nx, Ny, Nz, edge, k, 0.0, L, khat, ndir, T);
+}
+
+extern "C" fmmt_status fmmt_build_operator_lossy(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int64_t Nz, double edge,
+                                                 double k_re, double k_im, int64_t L, const double* khat,
+                                                 int64_t ndir, fmmt_c128* T) {
+  return build_operator_impl(ctx, Nx, Ny, Nz, edge, k_re, k_im, L, khat, ndir, T);
 }
 
 // ============================================================== FP64 helpers

@@ -66,6 +66,8 @@ fmmt_launch_count = _sig("fmmt_launch_count", i64, vp)
 fmmt_multipole_count = _sig("fmmt_multipole_count", C.c_int, C.c_double, C.c_double, C.c_double, i64p)
 fmmt_direction_grid = _sig("fmmt_direction_grid", C.c_int, i64, i64, vp, vp)
 fmmt_build_operator = _sig("fmmt_build_operator", C.c_int, vp, i64, i64, i64, C.c_double, C.c_double, i64, vp, i64, vp)
+fmmt_build_operator_lossy = _sig("fmmt_build_operator_lossy", C.c_int, vp, i64, i64, i64, C.c_double, C.c_double,
+                                 C.c_double, i64, vp, i64, vp)
 fmmt_compress = _sig("fmmt_compress", C.c_int, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_double, C.POINTER(vp))
 fmmt_op_import = _sig("fmmt_op_import", C.c_int, vp, C.c_int, i64, i64, i64, i64, i64p, C.POINTER(vp), i64, C.POINTER(vp))
 fmmt_op_destroy = _sig("fmmt_op_destroy", None, vp)
@@ -87,7 +89,7 @@ EXPORTED = [
     "fmmt_launch_count", "fmmt_multipole_count", "fmmt_direction_grid", "fmmt_build_operator", "fmmt_compress",
     "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_set_batch", "fmmt_translate",
     "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
-    "fmmt_translate_multi", "fmmt_translate_sum_multi",
+    "fmmt_translate_multi", "fmmt_translate_sum_multi", "fmmt_build_operator_lossy",
 ]
 
 
@@ -199,6 +201,11 @@ class Context:
         khat = np.ascontiguousarray(khat, dtype=np.float64)
         _check(fmmt_build_operator(self.h, Nx, Ny, Nz, edge, k, L, khat.ctypes.data, len(khat), _ptr(out)),
                self.h, "fmmt_build_operator")
+
+    def build_operator_lossy(self, Nx, Ny, Nz, edge, k: complex, L, khat: np.ndarray, out):
+        khat = np.ascontiguousarray(khat, dtype=np.float64)
+        _check(fmmt_build_operator_lossy(self.h, Nx, Ny, Nz, edge, float(k.real), float(k.imag), L, khat.ctypes.data,
+                                         len(khat), _ptr(out)), self.h, "fmmt_build_operator_lossy")
 
     def compress(self, T, n, ndir, fmt, tol, dir_begin=0, dir_count=None) -> "Op":
         fmt = FORMATS[fmt] if isinstance(fmt, str) else fmt

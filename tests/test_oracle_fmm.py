@@ -192,3 +192,73 @@ def test_direction_mode_rank_is_L_plus_1_squared():
     r = (c.L + 1) ** 2
     assert s[r - 1] / s[0] > 0.1
     assert s[r] / s[0] < 1e-12
+
+
+# ---------------------------------------------------------------- lossy media
+def test_medium_wavenumber_sign_and_lossless_limit():
+    """k = k0 sqrt(eps_r), Im k <= 0 for eps_r = eps' - j eps'' (e^{+j omega t}); Table IV media."""
+    k = fmm.medium_wavenumber(2 - 1j)
+    assert k.imag < 0 and abs(k * k - (2 * np.pi) ** 2 * (2 - 1j)) < 1e-12
+    assert abs(fmm.medium_wavenumber(1.0) - 2 * np.pi) < 1e-15
+    # h^(2) decays with R in a lossy medium
+    assert abs(fmm.sph_hankel2(0, k * 10.0)) < abs(fmm.sph_hankel2(0, k * 5.0)) * np.exp(-4.0)
+
+
+def test_hankel_complex_argument():
+    """Closed forms and the upward recurrence at complex z (lossy kR)."""
+    z = np.array([0.7 - 0.1j, np.pi - 0.5j, 5.3 - 1.2j, 11.33 - 2.6j, 22.6 - 5.1j])
+    np.testing.assert_allclose(fmm.sph_hankel2(0, z), 1j * np.exp(-1j * z) / z, rtol=1e-11)
+    np.testing.assert_allclose(fmm.sph_hankel2(1, z), np.exp(-1j * z) * (1j - z) / z ** 2, rtol=1e-11)
+    h = [1j * np.exp(-1j * z) / z, np.exp(-1j * z) * (1j - z) / z ** 2]
+    for l in range(1, 20):
+        h.append((2 * l + 1) / z * h[l] - h[l - 1])
+        np.testing.assert_allclose(fmm.sph_hankel2(l + 1, z), h[l + 1], rtol=1e-9)
+    # small losses: the series agrees with SciPy's j_l - i y_l (no cancellation there)
+    from scipy import special as sp
+    zs = np.array([3.0 - 0.01j, 7.5 - 0.05j, 15.0 - 0.1j])
+    for l in range(0, 15):
+        np.testing.assert_allclose(fmm.sph_hankel2(l, zs), sp.spherical_jn(l, zs) - 1j * sp.spherical_yn(l, zs),
+                                   rtol=1e-10)
+    # strong losses: |h_l^(2)(z)| decays like e^{Im z} (no e^{|Im z|} garbage)
+    zl = 40.0 - 30.0j
+    assert abs(fmm.sph_hankel2(10, zl)) < 10 * np.exp(-30.0)
+
+
+@pytest.mark.parametrize("eps_r", [2 - 1j, 2 - 2j])
+def test_green_function_identity_lossy(eps_r):
+    """The plane-wave identity of eq. (5)-(7) with a complex wavenumber:
+    sum_p w_p e^{-jk k_p.d} T~(X, k_p) = 4 pi h_0^(2)(k|X+d|), L from |k| (P:63, 5 digits)."""
+    k = fmm.medium_wavenumber(eps_r)
+    edge, digits = 0.5, 5
+    L = fmm.multipole_count(abs(k), edge, digits)
+    khat, w, _, _ = fmm.direction_grid(L, 2 * (L + 1))
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for u in [(4, 0, 0), (3, 2, 0), (2, 2, 3)]:
+        X = np.array(u, float) * edge
+        for _ in range(3):
+            d = rng.uniform(-0.3, 0.3, 3) * edge
+            t = _t_scalar(X, khat, k, L)
+            lhs = np.sum(w * np.exp(-1j * k * (khat @ d)) * t)
+            r = np.linalg.norm(X + d)
+            rhs = 4 * np.pi * 1j * np.exp(-1j * k * r) / (k * r)
+            worst = max(worst, abs(lhs - rhs) / abs(rhs))
+    assert worst < 10 * 10.0 ** (-digits)
+
+
+def test_lossy_operator_grid_reduces_to_lossless():
+    """OperatorGrid with Im k -> 0 equals the real-k operator; lossy FFT'ed operator has
+    a lower numerical multilinear rank (Table IV: savings rise with loss)."""
+    from oracle import decomp
+    c = config(1)
+    khat, _, _, _ = fmm.direction_grid(c.L, c.nphi)
+    g0 = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L)
+    g1 = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, complex(c.k, -1e-14), c.L)
+    assert np.max(np.abs(g0.spatial(khat[5]) - g1.spatial(khat[5]))) < 1e-12
+    kl = fmm.medium_wavenumber(2 - 8j)
+    gl = fmm.OperatorGrid(8, 8, 8, 0.5, kl, fmm.multipole_count(abs(kl), 0.5, 3))
+    kk = fmm.medium_wavenumber(2.0)
+    gk = fmm.OperatorGrid(8, 8, 8, 0.5, kk, fmm.multipole_count(abs(kk), 0.5, 3))
+    rl = decomp.tucker_svd(fmm.fft_operator_3d(gl, khat[5]), 1e-4).ranks
+    rk = decomp.tucker_svd(fmm.fft_operator_3d(gk, khat[5]), 1e-4).ranks
+    assert sum(rl) < sum(rk)
