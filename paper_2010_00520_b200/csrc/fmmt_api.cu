@@ -245,6 +245,8 @@ struct fmmt_op {
   std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
   int64_t pack_bytes = 0;
   int64_t w_ncomp = 1;                         // signature components W is allocated for
+  float2* zscr = nullptr;                      // n3 = 64 tensor-core z-stage: even-pass partials (batch)
+  int64_t zscr_elems = 0;
   // workspace
   int64_t PB = 0;
   int64_t sigtmp_elems = 0;
@@ -298,6 +300,7 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->d_rank) cudaFree(op->d_rank);
   if (op->tbar1) cudaFree(op->tbar1);
   if (op->E) cudaFree(op->E);
+  if (op->zscr) cudaFree(op->zscr);
   if (op->tbar1_pk) cudaFree(op->tbar1_pk);
   if (op->E_pk) cudaFree(op->E_pk);
   for (auto pk : op->arr_pk)
@@ -482,6 +485,8 @@ static void tucker_chain(fmmt_op* op, Batch& b) {
   add_gemm(op, b, sb, "restore_mode2");
 }
 
+static fmmt_status ensure_zscr(fmmt_op* op);
+
 static fmmt_status build_plans(fmmt_op* op) {
   free_workspace(op);
   op->descs.clear();
@@ -576,6 +581,12 @@ static fmmt_status build_plans(fmmt_op* op) {
     }
     op->batches.push_back(b);
   }
+  if (op->zscr) {   // batch size may have changed
+    cudaFree(op->zscr);
+    op->zscr = nullptr;
+    op->zscr_elems = 0;
+  }
+  if ((st = ensure_zscr(op))) return st;
   if (!op->descs.empty()) {
     FMMT_CUDA(op->ctx, cudaMalloc(&op->d_descs, op->descs.size() * sizeof(GemmDesc)));
     FMMT_CUDA(op->ctx, cudaMemcpy(op->d_descs, op->descs.data(), op->descs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
@@ -590,8 +601,11 @@ template <int BN>
 static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
   using Cfg = fmmt::TcGemmCfg<BN, TC_G>;
   FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN, TC_G>, Cfg::SMEM));
-  dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
-  fmmt::k_tc_cgemm<BN, TC_G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(d);
+  const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
+  // 2 CTAs per SM resident (smem, TMEM); each walks total / grid tiles
+  const int64_t cap = (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, cap));
+  fmmt::k_tc_cgemm<BN, TC_G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, (int)total);
   return FMMT_OK;
 }
 
@@ -703,7 +717,8 @@ static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& 
   constexpr int BN = N3 * ND < 16 ? 16 : N3 * ND;
   constexpr int G = 1;   // 2 = even/odd kz split over two thread groups (measured slower: 1 CTA/SM by registers)
   using Cfg = fmmt::TcGemmCfg<BN, G>;
-  dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)((nq + ND - 1) / ND));
+  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)((nq + ND - 1) / ND);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm));
   if (mode == fmmt::Z_RESTORE) {
     if constexpr (ND == 1) {
       FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G>, Cfg::SMEM));
@@ -745,6 +760,34 @@ static fmmt_status launch_tc1_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a)
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0,
                             int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
+  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 == 64) {
+    // tensor-core z-stage for n3 = 64: two parity passes, even-pass partial in op->zscr
+    ZArgs a;
+    fill_zargs(op, a);
+    a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
+    a.ncomp = ncomp;
+    a.p0 = p0;
+    a.G = a.G + (int64_t)qoff * a.g_stride;
+    if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
+    a.Tout = Tout;
+    if (mode != fmmt::Z_RESTORE && (!op->zscr || op->zscr_elems < (int64_t)nq * ncomp * (op->n3 / 2) * a.n12))
+      return set_err(ctx, FMMT_E_STATE, "z scratch not allocated");
+    static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
+                                   "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
+    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
+    using Cfg = fmmt::TcGemmCfg<32, 1>;
+    const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm));
+    if (mode == fmmt::Z_RESTORE) {
+      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z64<fmmt::Z_RESTORE>, Cfg::SMEM));
+      fmmt::k_tc_conv_z64<fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, op->zscr, nq);
+    } else {
+      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z64<fmmt::Z_LOWRANK>, Cfg::SMEM));
+      fmmt::k_tc_conv_z64<fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, op->zscr, nq);
+    }
+    FMMT_CUDA(ctx, cudaGetLastError());
+    return FMMT_OK;
+  }
   if (ctx->gemm_impl >= 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
     fill_zargs(op, a);
@@ -798,6 +841,21 @@ static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
   return FMMT_OK;
 }
 
+// Scratch of the n3 = 64 tensor-core z-stage: one batch of half-padded lines per component.
+static fmmt_status ensure_zscr(fmmt_op* op) {
+  if (op->n3 != 64 || op->format == FMMT_DENSE) return FMMT_OK;
+  const int64_t need = op->PB * op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2;
+  if (op->zscr && op->zscr_elems >= need) return FMMT_OK;
+  if (op->zscr) {
+    cudaFree(op->zscr);
+    op->ws_bytes -= op->zscr_elems * 8;
+    op->zscr = nullptr;
+  }
+  fmmt_status st = cmalloc(op, &op->zscr, need);
+  if (!st) op->zscr_elems = need;
+  return st;
+}
+
 // W (the half-padded spectra of every direction and component) sized for ncomp components.
 static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
   if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
@@ -813,7 +871,9 @@ static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
     op->W = nullptr;
   }
   op->w_ncomp = std::max<int64_t>(ncomp, op->w_ncomp);
-  return cmalloc(op, &op->W, op->w_ncomp * elems);
+  fmmt_status st = cmalloc(op, &op->W, op->w_ncomp * elems);
+  if (st) return st;
+  return ensure_zscr(op);
 }
 
 static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int ncomp = 1) {
@@ -965,6 +1025,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
   if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
     ncclUniqueId id;

@@ -71,6 +71,11 @@ struct TcGemmCfg {
 // in separate accumulators, and the chunk results are summed in FP32 registers
 // (round-to-nearest).  Two slots alternate so chunk k+1's MMAs overlap the
 // drain of chunk k.  A thread drains its row's columns [c0, c0 + NRG).
+struct TcCursor {
+  int c = 0;   // chunks issued by this CTA so far
+  int g = 0;   // TMEM flush groups used by this CTA so far
+};
+
 template <int NR, int NRG>
 __device__ __forceinline__ void tc_flush(uint32_t tslot_addr, int c0, float (&acc)[NRG]) {
 #pragma unroll
@@ -92,13 +97,15 @@ __device__ __forceinline__ void tc_flush(uint32_t tslot_addr, int c0, float (&ac
 // the tile, re/im interleaved) = A[m0:m0+128, :] . B[:, n0:n0+BN] over all of K.
 // Called by all 128 G threads.  bar[0..1]: MMA commits per stage; bar[2..3]:
 // packed-A bulk copies per stage.
-// cb: this call's first global chunk number (a multiple of TC_FC; 0 for the first call of a CTA):
-// ring stages, barrier phases and TMEM flush groups continue across calls.  Returns the next cb.
+// Per-CTA pipeline position, continued across calls (several tiles per CTA, two passes of the
+// n3 = 64 z-stage): c = chunks issued so far (ring stage c % NS, barrier phase (c / NS) & 1,
+// exact - a gap would desynchronise the per-stage barrier phases), g = TMEM flush groups so far
+// (slot g & 1, tfree phase (g / 2) & 1; every call starts a fresh group).
 template <int BN, int G>
-__device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
+__device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
                                            const float2* __restrict__ B, int m0, int n0, uint8_t* tcsm,
                                            uint64_t* bar, uint32_t tmem,
-                                           float (&acc)[TcGemmCfg<BN, G>::NRG], int cb = 0) {
+                                           float (&acc)[TcGemmCfg<BN, G>::NRG], TcCursor& cur) {
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int BM = TC_BM, BK = TC_BK, NR = Cfg::NR, NRG = Cfg::NRG, NT = Cfg::NT;
   constexpr int BITEMS = Cfg::BITEMS;
@@ -129,7 +136,7 @@ __device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __re
   // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
   auto issue = [&](int c) {
     const int k0 = c * BK;
-    const int cs = (cb + c) % TC_NS;
+    const int cs = (cur.c + c) % TC_NS;
     const uint32_t st = sbase + cs * Cfg::STAGE;
     if (apack) {
       if (tid == 0) {
@@ -193,12 +200,13 @@ __device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __re
   uint64_t* abar = bar + TC_NS;
   uint64_t* full = bar + 2 * TC_NS;
   uint64_t* tfree = bar + 3 * TC_NS;
-  int flushed = cb / TC_FC;              // flush groups (global numbering) already drained into acc
+  int flushed = 0;                       // this call's flush groups already drained into acc
   auto drain_complete = [&](int done) {  // this call's chunks [0, done) have completed MMAs
-    for (; (flushed + 1) * TC_FC <= cb + done; ++flushed) {
-      tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+    for (; (flushed + 1) * TC_FC <= done; ++flushed) {
+      const int gid = cur.g + flushed;
+      tc_flush<NR, NRG>(twarp + (gid & 1) * 2 * NR, c0, acc);
       tc::fence_before_sync();
-      tc::mbar_arrive(&tfree[flushed & 1]);
+      tc::mbar_arrive(&tfree[gid & 1]);
     }
   };
   constexpr int D = TC_NS - 2;           // copy prefetch distance (chunks)
@@ -208,7 +216,7 @@ __device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __re
     else tc::cp_async_commit();
   }
   for (int kc = 0; kc < nk; ++kc) {
-    const int gc = cb + kc;                // global chunk number
+    const int gc = cur.c + kc;             // CTA-wide chunk number (stage, barrier phases)
     const int s = gc % TC_NS;
     const uint32_t ph = (gc / TC_NS) & 1;
     if (kc >= 2) {
@@ -272,8 +280,8 @@ __device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __re
     tc::mbar_arrive(&full[s]);
     if (tid == 0) {
       tc::mbar_wait(&full[s], ph);                    // all 128 threads' operands of chunk kc are in place
-      const int g = gc / TC_FC;
-      const bool fresh = gc % TC_FC == 0;             // first chunk of a flush group
+      const int g = cur.g + kc / TC_FC;               // CTA-wide flush group (TMEM slot, tfree phase)
+      const bool fresh = kc % TC_FC == 0;             // first chunk of a flush group
       if (fresh && g >= 2) tc::mbar_wait(&tfree[g & 1], ((g >> 1) - 1) & 1);   // group g-2 drained
       tc::fence_after_sync();
       const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
@@ -292,16 +300,18 @@ __device__ __forceinline__ int tc_mainloop(const GemmDesc& d, const float2* __re
   }
   tc::cp_async_wait<0>();
   // drain the remaining flush groups (the last one possibly partial)
-  tc::mbar_wait(&mmab[(cb + nk - 1) % TC_NS], ((cb + nk - 1) / TC_NS) & 1);
+  tc::mbar_wait(&mmab[(cur.c + nk - 1) % TC_NS], ((cur.c + nk - 1) / TC_NS) & 1);
   tc::fence_after_sync();
   drain_complete(nk);
-  if (flushed * TC_FC < cb + nk) {
-    tc_flush<NR, NRG>(twarp + (flushed & 1) * 2 * NR, c0, acc);
+  if (flushed * TC_FC < nk) {                        // the last, partial group
+    const int gid = cur.g + flushed;
+    tc_flush<NR, NRG>(twarp + (gid & 1) * 2 * NR, c0, acc);
     tc::fence_before_sync();
-    tc::mbar_arrive(&tfree[flushed & 1]);            // (keeps tfree phases aligned for a next call)
+    tc::mbar_arrive(&tfree[gid & 1]);                // (keeps tfree phases aligned for a next call)
     ++flushed;
   }
-  return flushed * TC_FC;
+  cur.c += nk;
+  cur.g += flushed;
 }
 
 // TMEM allocation + stage barriers (all threads call; warp 0 allocates).
@@ -328,39 +338,44 @@ __device__ __forceinline__ void tc_teardown(uint32_t tmem) {
   if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
+// A CTA walks the launch's tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... (flattened over
+// (tile, sub-batch, descriptor)), reusing its TMEM allocation and barriers; the chunk numbering
+// continues across tiles (TcCursor), so the ring and the TMEM slots stay consistent.
 template <int BN, int G>
-__global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict__ descs, int maxtiles, int maxsub,
+                                                      int total) {
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int BM = TC_BM, NRG = Cfg::NRG;
   extern __shared__ __align__(1024) uint8_t tcsm[];
   __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
   __shared__ uint32_t tslot;
 
-  const GemmDesc d = descs[blockIdx.z];
-  const int sub = blockIdx.y;
-  if (sub >= d.batch) return;
-  const int tiles_m = (d.m + BM - 1) / BM;
-  const int tiles_n = (d.n + BN - 1) / BN;
-  const int tile = blockIdx.x;
-  if (tile >= tiles_m * tiles_n) return;
-  const int m0 = (tile % tiles_m) * BM;
-  const int n0 = (tile / tiles_m) * BN;
-  const float2* __restrict__ A = d.A + (int64_t)sub * d.sA;
-  const float2* __restrict__ B = d.B + (int64_t)sub * d.sB;
-  float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
-
   const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
-  float acc[NRG];
-  tc_mainloop<BN, G>(d, A, B, m0, n0, tcsm, bar, tmem, acc);
-
-  const int gm = m0 + (threadIdx.x & 127);
-  const int nb = n0 + (threadIdx.x >> 7) * (BN / G);
-  if (gm < d.m) {
-    const int64_t crow = c_row(d, gm);
+  TcCursor cur;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int x = t % maxtiles;
+    const int sub = (t / maxtiles) % maxsub;
+    const GemmDesc d = descs[t / (maxtiles * maxsub)];
+    if (sub >= d.batch) continue;                      // uniform over the CTA
+    const int tiles_m = (d.m + BM - 1) / BM;
+    const int tiles_n = (d.n + BN - 1) / BN;
+    if (x >= tiles_m * tiles_n) continue;
+    const int m0 = (x % tiles_m) * BM;
+    const int n0 = (x / tiles_m) * BN;
+    const float2* __restrict__ A = d.A + (int64_t)sub * d.sA;
+    const float2* __restrict__ B = d.B + (int64_t)sub * d.sB;
+    float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
+    float acc[NRG];
+    tc_mainloop<BN, G>(d, A, B, m0, n0, tcsm, bar, tmem, acc, cur);
+    const int gm = m0 + (threadIdx.x & 127);
+    const int nb = n0 + (threadIdx.x >> 7) * (BN / G);
+    if (gm < d.m) {
+      const int64_t crow = c_row(d, gm);
 #pragma unroll
-    for (int j = 0; j < BN / G; ++j) {
-      const int gn = nb + j;
-      if (gn < d.n) C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+      for (int j = 0; j < BN / G; ++j) {
+        const int gn = nb + j;
+        if (gn < d.n) C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+      }
     }
   }
   tc_teardown<Cfg::TMEM_COLS>(tmem);
@@ -389,62 +404,150 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
   __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
   __shared__ uint32_t tslot;
 
-  const int q0 = blockIdx.y * ND;
-  const int p0 = a.p0 + q0;
-  const int nd = min(ND, nq - q0);
-  const int m0 = blockIdx.x * TC_BM;
-  GemmDesc d;
-  d.m = (int)a.n12;
-  d.n = nd * N3;
-  d.k = a.rank_p ? a.rank_p[p0] : a.rank;
-  d.batch = 1;
-  d.a_s0 = 1; d.a_s1 = 0; d.a_div = 1 << 30; d.a_sk = a.n12;
-  d.b_sk = a.v_sc; d.b_sn = a.v_sk;     // ND > 1: v_stride == N3 * v_sk (checked on the host)
-  d.b_eo = (G == 2) ? 1 : 0;
-  d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
-  d.sA = d.sB = d.sC = 0;
-  d.Ap = a.Gp;                          // pre-split shared G (TT-4D T1), or nullptr
-  d.a_nkc = (d.k + TC_BK - 1) / TC_BK;
-  const float2* A = a.G + (int64_t)q0 * a.g_stride;
-  const float2* B = a.V + (a.v_off ? a.v_off[p0] : (int64_t)q0 * a.v_stride);
-
-  const int row = threadIdx.x & 127, grp = threadIdx.x >> 7;
-  const int64_t ij = m0 + row;
-  const bool valid = ij < a.n12;
-
+  const int tiles_m = (int)((a.n12 + TC_BM - 1) / TC_BM);
+  const int total = tiles_m * ((nq + ND - 1) / ND);
+  const int row = threadIdx.x & 127;
   const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
-  float acc[Cfg::NRG];
-  tc_mainloop<BN, G>(d, A, B, m0, 0, tcsm, bar, tmem, acc);
+  TcCursor cur;
+  // tiles t = (m-tile, direction group), walked by this CTA with one TMEM allocation
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int q0 = (t / tiles_m) * ND;
+    const int p0 = a.p0 + q0;
+    const int nd = min(ND, nq - q0);
+    const int m0 = (t % tiles_m) * TC_BM;
+    GemmDesc d;
+    d.m = (int)a.n12;
+    d.n = nd * N3;
+    d.k = a.rank_p ? a.rank_p[p0] : a.rank;
+    d.batch = 1;
+    d.a_s0 = 1; d.a_s1 = 0; d.a_div = 1 << 30; d.a_sk = a.n12;
+    d.b_sk = a.v_sc; d.b_sn = a.v_sk;     // ND > 1: v_stride == N3 * v_sk (checked on the host)
+    d.b_eo = 0;
+    d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
+    d.sA = d.sB = d.sC = 0;
+    d.Ap = a.Gp;                          // pre-split shared G (TT-4D T1), or nullptr
+    d.a_nkc = (d.k + TC_BK - 1) / TC_BK;
+    const float2* A = a.G + (int64_t)q0 * a.g_stride;
+    const float2* B = a.V + (a.v_off ? a.v_off[p0] : (int64_t)q0 * a.v_stride);
+    const int64_t ij = m0 + row;
+    const bool valid = ij < a.n12;
 
-  if constexpr (MODE == Z_RESTORE) {
-    if (valid) {
+    float acc[Cfg::NRG];
+    tc_mainloop<BN, G>(d, A, B, m0, 0, tcsm, bar, tmem, acc, cur);
+
+    if constexpr (MODE == Z_RESTORE) {
+      if (valid) {
 #pragma unroll
-      for (int j = 0; j < BN / G; ++j) {
-        const int n = grp * (BN / G) + j;                       // column in (even, odd) order
-        const int kz = (G == 2) ? (n < N3 / 2 ? 2 * n : 2 * (n - N3 / 2) + 1) : n;
-        if (kz < N3) a.Tout[(int64_t)kz * a.n12 + ij] = make_float2(acc[2 * j], acc[2 * j + 1]);
+        for (int kz = 0; kz < N3; ++kz) a.Tout[(int64_t)kz * a.n12 + ij] = make_float2(acc[2 * kz], acc[2 * kz + 1]);
       }
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int dq = 0; dq < ND; ++dq) {
-      if (dq >= nd) continue;
-      for (int cc = 0; cc < a.ncomp; ++cc) {   // signature components share the restored line
-        float2* Wl = a.W + ((int64_t)(q0 + dq) * a.ncomp + cc) * Nz * a.n12 + (valid ? ij : 0);
-        float2 f[N3];
+      for (int dq = 0; dq < ND; ++dq) {
+        if (dq >= nd) continue;
+        for (int cc = 0; cc < a.ncomp; ++cc) {   // signature components share the restored line
+          float2* Wl = a.W + ((int64_t)(q0 + dq) * a.ncomp + cc) * Nz * a.n12 + (valid ? ij : 0);
+          float2 f[N3];
 #pragma unroll
-        for (int z = 0; z < Nz; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
-        fft_reg<N3, false, true>(f);
+          for (int z = 0; z < Nz; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
+          fft_reg<N3, false, true>(f);
 #pragma unroll
-        for (int kz = 0; kz < N3; ++kz)
-          f[kz] = cmul(make_float2(acc[2 * (dq * N3 + kz)], acc[2 * (dq * N3 + kz) + 1]), f[kz]);
-        fft_reg<N3, true, false>(f);
-        if (valid) {
+          for (int kz = 0; kz < N3; ++kz)
+            f[kz] = cmul(make_float2(acc[2 * (dq * N3 + kz)], acc[2 * (dq * N3 + kz) + 1]), f[kz]);
+          fft_reg<N3, true, false>(f);
+          if (valid) {
 #pragma unroll
-          for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
+            for (int z = 0; z < Nz; ++z) Wl[(int64_t)z * a.n12] = f[z];
+          }
         }
       }
     }
+  }
+  tc_teardown<Cfg::TMEM_COLS>(tmem);
+}
+
+// ---------------------------------------------------------------- k_tc_conv_z64
+// z-stage for n3 = 64 (configs 4, 5) on the tensor cores.  A 64-column tile would need
+// 512 TMEM columns and 128 accumulator registers per thread, so the kz range is split by
+// parity (B columns in (even, odd) order) into two 32-column passes over the same rows:
+//   A^[2m]   = DFT_32(x)[m],                A^[2m+1] = DFT_32(x[z] W_64^z)[m]      (x: z < 32)
+//   y[z]     = IDFT_32(T_even A^_even)[z] + W_64^{-z} IDFT_32(T_odd A^_odd)[z]      (z < 32)
+// (the unnormalised length-64 transforms of eq. (5), pruned input, truncated output).  The
+// even-pass partial y goes to a scratch line S and is added in the odd pass.
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restrict__ S, int nq) {
+  constexpr int N3 = 64, H = 32, BN = 32;
+  using Cfg = TcGemmCfg<BN, 1>;
+  extern __shared__ __align__(1024) uint8_t tcsm[];
+  __shared__ __align__(8) uint64_t bar[3 * TC_NS + 2];
+  __shared__ uint32_t tslot;
+
+  const int tiles_m = (int)((a.n12 + TC_BM - 1) / TC_BM);
+  const int total = tiles_m * nq;
+  const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
+  TcCursor cur;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+  const int q = t / tiles_m;
+  const int p = a.p0 + q;
+  const int m0 = (t % tiles_m) * TC_BM;
+  GemmDesc d;
+  d.m = (int)a.n12;
+  d.n = N3;
+  d.k = a.rank_p ? a.rank_p[p] : a.rank;
+  d.batch = 1;
+  d.a_s0 = 1; d.a_s1 = 0; d.a_div = 1 << 30; d.a_sk = a.n12;
+  d.b_sk = a.v_sc; d.b_sn = a.v_sk;
+  d.b_eo = 1;                              // column j < 32 -> kz = 2j, j >= 32 -> kz = 2(j-32)+1
+  d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
+  d.sA = d.sB = d.sC = 0;
+  d.Ap = a.Gp;
+  d.a_nkc = (d.k + TC_BK - 1) / TC_BK;
+  const float2* A = a.G + (int64_t)q * a.g_stride;
+  const float2* B = a.V + (a.v_off ? a.v_off[p] : (int64_t)q * a.v_stride);
+
+  const int row = threadIdx.x;
+  const int64_t ij = m0 + row;
+  const bool valid = ij < a.n12;
+
+  float acc[2 * BN];
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    tc_mainloop<BN, 1>(d, A, B, m0, h * H, tcsm, bar, tmem, acc, cur);   // T_p[ij, 2m + h]
+    if constexpr (MODE == Z_RESTORE) {
+      if (valid) {
+#pragma unroll
+        for (int m = 0; m < H; ++m) a.Tout[(int64_t)(2 * m + h) * a.n12 + ij] = make_float2(acc[2 * m], acc[2 * m + 1]);
+      }
+    } else {
+      for (int cc = 0; cc < a.ncomp; ++cc) {
+        const int64_t line = ((int64_t)q * a.ncomp + cc) * H * a.n12 + (valid ? ij : 0);
+        float2* Wl = a.W + line;
+        float2* Sl = S + line;
+        float2 f[H];
+#pragma unroll
+        for (int z = 0; z < H; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
+        if (h) {
+#pragma unroll
+          for (int z = 1; z < H; ++z) f[z] = cmul(f[z], twc<N3, false>(z));
+        }
+        fft_reg<H, false, false>(f);
+#pragma unroll
+        for (int m = 0; m < H; ++m) f[m] = cmul(make_float2(acc[2 * m], acc[2 * m + 1]), f[m]);
+        fft_reg<H, true, false>(f);
+        if (valid) {
+          if (h == 0) {
+#pragma unroll
+            for (int z = 0; z < H; ++z) Sl[(int64_t)z * a.n12] = f[z];
+          } else {
+#pragma unroll
+            for (int z = 0; z < H; ++z) {
+              const float2 odd = z ? cmul(f[z], twc<N3, true>(z)) : f[z];
+              Wl[(int64_t)z * a.n12] = cadd(Sl[(int64_t)z * a.n12], odd);
+            }
+          }
+        }
+      }
+    }
+  }
   }
   tc_teardown<Cfg::TMEM_COLS>(tmem);
 }
