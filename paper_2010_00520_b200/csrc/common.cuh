@@ -29,6 +29,15 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+// b * w = b.x (w.x, w.y) + b.y (-w.y, w.x): one FMUL2 + one FFMA2 (w a compile-time twiddle,
+// so (-w.y, w.x) is a constant pair; for variable w the negation costs one FADD).
+__device__ __forceinline__ float2 cmul2(float2 b, float2 w) {
+  uint64_t t, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2(make_float2(b.x, b.x))), "l"(pk2(w)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(make_float2(b.y, b.y))), "l"(pk2(make_float2(-w.y, w.x))),
+      "l"(t));
+  return upk2(r);
+}
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 // acc += a * b  (4 FFMA)
 __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {

@@ -27,7 +27,7 @@ __device__ __forceinline__ float2 twmul(float2 b, int j) {
     // forward: * (-i) = (y, -x); inverse: * (+i) = (-y, x)
     return INV ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
   }
-  return cmul(b, twc<SPAN, INV>(j));
+  return cmul2(b, twc<SPAN, INV>(j));
 }
 
 // Radix-2 butterfly stages of span SPAN, 2 SPAN, ..., M (compile-time recursion, so

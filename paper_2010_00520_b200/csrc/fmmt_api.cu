@@ -29,6 +29,7 @@
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
 #include "kernels_tcgemm_v1.cuh"
+#include "kernels_tcws.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -598,7 +599,18 @@ static fmmt_status build_plans(fmmt_op* op) {
 constexpr int TC_G = 1;   // thread groups per tensor-core CTA (2 = 256 threads: measured slower)
 
 template <int BN>
+static fmmt_status launch_tcw_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
+  constexpr int SMEM = fmmt::TcwCfg<BN>::SMEM;
+  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_cgemm<BN>, SMEM));
+  const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // 1 CTA / SM
+  fmmt::k_tcw_cgemm<BN><<<grid, 256, SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, (int)total);
+  return FMMT_OK;
+}
+
+template <int BN>
 static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
+  if (ctx->warp_specialised) return launch_tcw_bn<BN>(ctx, L, d);
   using Cfg = fmmt::TcGemmCfg<BN, TC_G>;
   FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN, TC_G>, Cfg::SMEM));
   const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
@@ -732,10 +744,27 @@ static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& 
   return FMMT_OK;
 }
 
+template <int N3>
+static fmmt_status launch_tcw_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
+  constexpr int SMEM = fmmt::TcwCfg<(N3 < 16 ? 16 : N3)>::SMEM;
+  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));
+  if (mode == fmmt::Z_RESTORE) {
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_conv_z<N3, fmmt::Z_RESTORE>, SMEM));
+    fmmt::k_tcw_conv_z<N3, fmmt::Z_RESTORE><<<grid, 256, SMEM, ctx->stream>>>(a, nq);
+  } else {
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_conv_z<N3, fmmt::Z_LOWRANK>, SMEM));
+    fmmt::k_tcw_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 256, SMEM, ctx->stream>>>(a, nq);
+  }
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
 // Directions per z tile: > 1 only when all directions share G (TT-4D's T1) and the
 // V_q of consecutive directions are contiguous ([q][kz][c]), up to 2 n3 = 64 columns.
 template <int N3>
 static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
+  if (ctx->warp_specialised) return launch_tcw_z<N3>(ctx, mode, nq, a);
   const bool shareable = a.g_stride == 0 && !a.v_off && a.v_stride == (int64_t)N3 * a.v_sk && mode != fmmt::Z_RESTORE;
   if (shareable && N3 <= 32 && ctx->z_multidir) {
     constexpr int ND = 64 / N3 > 4 ? 4 : 64 / N3;
@@ -1026,6 +1055,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
   if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("FMMT_WS")) ctx->warp_specialised = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
     ncclUniqueId id;

@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
           fft_reg<N3, false, true>(f);
 #pragma unroll
           for (int kz = 0; kz < N3; ++kz)
-            f[kz] = cmul(make_float2(acc[2 * (dq * N3 + kz)], acc[2 * (dq * N3 + kz) + 1]), f[kz]);
+            f[kz] = cmul2(f[kz], make_float2(acc[2 * (dq * N3 + kz)], acc[2 * (dq * N3 + kz) + 1]));
           fft_reg<N3, true, false>(f);
           if (valid) {
 #pragma unroll
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
         }
         fft_reg<H, false, false>(f);
 #pragma unroll
-        for (int m = 0; m < H; ++m) f[m] = cmul(make_float2(acc[2 * m], acc[2 * m + 1]), f[m]);
+        for (int m = 0; m < H; ++m) f[m] = cmul2(f[m], make_float2(acc[2 * m], acc[2 * m + 1]));
         fft_reg<H, true, false>(f);
         if (valid) {
           if (h == 0) {
