@@ -17,6 +17,7 @@ decomp     Alg. 1 Tucker-SVD, Alg. 2 H-Tucker-SVD, Alg. 3 TT-SVD, truncation rul
 restore    dense eqs. (8), (9), (11), (13), (14) and the slice chains of Figs. 3-4
 translate  eq. (5) by brute-force circular direct sum and by FP64 FFT; eq. (6) sum
 memory     compressed-memory count
+aggregate  eq. (4) aggregation and eq. (6) disaggregation around eq. (5)
 
 Parity status: every function is pinned by a `-m "not gpu"` test in
 tests/test_oracle_*.py; none is "parity unpinned".

@@ -7,14 +7,15 @@ on the GPU in FP64 (Alg. 1-3, fmmt_compress) for the five formats; the ranks and
 saving are printed next to the paper's Table II ranks (context: the paper's operators come from
 its own sphere geometry and its rank rule; readings Q7/Q8 of DESIGN.md differ).
 
-    python scripts/table2_sweep.py [n ...]        (default 32 64 128) -> one JSON line per n
+    python scripts/table2_sweep.py [--gamma G] [n ...]   (default gamma 1e-6, n = 32 64) -> one JSON line per n
+
+n = 128 (32 lambda) is outside the translate path (n3 <= 64) and is not swept.
 """
 import json
 import math
 import sys
 import time
 
-import numpy as np
 import torch
 
 sys.path.insert(0, ".")
@@ -28,9 +29,13 @@ PAPER = {  # Table II: TT-3D rmax, Tucker-3D rmax, TT-4D (r1, r2), T
 
 
 def main():
-    ns = [int(x) for x in sys.argv[1:]] or [32, 64, 128]
+    args = sys.argv[1:]
+    gamma = 1e-6
+    if args[:1] == ["--gamma"]:
+        gamma, args = float(args[1]), args[2:]
+    ns = [int(x) for x in args] or [32, 64]
     ctx = fmmt.Context(0, torch.cuda.current_stream().cuda_stream)
-    edge, digits, gamma = 0.5, 5, 1e-6
+    edge, digits = 0.5, 5
     k = 2 * math.pi
     L = fmmt.multipole_count(k, edge, digits)
     khat, _ = fmmt.direction_grid(L, 2 * L + 1)
