@@ -256,6 +256,39 @@ fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, co
                                     fmmt_c64* sum_out_host, int64_t ndir,
                                     int64_t Nx, int64_t Ny, int64_t Nz);
 
+/* ------------------------------------------- around the translation
+ *
+ * Aggregation, eq. (4):  sig[p][c][v] = sum_{n in box v} P[p][n][c] * I[n],
+ * zero for an empty box.  Disaggregation, eq. (6), with P- = conj(P+):
+ *     y[m] = sum_p w[p] sum_c conj(P[p][m][c]) * B[p][c][v(m)].
+ * Arguments (all device memory, caller-owned; the library only reads P, I, B, w, box_ptr):
+ *   P        complex64 [ndir][N][ncomp]: far-field patterns P+(k_p, b_n), components
+ *            (theta, phi, ...) fastest; ncomp in [1, 16]
+ *   I        complex64 [N]: basis-function coefficients
+ *   box_ptr  int64 [K+1], K = Nx Ny Nz: the basis functions of box v (linear index
+ *            x + Nx (y + Ny z)) are n in [box_ptr[v], box_ptr[v+1]); box_ptr[0] = 0,
+ *            nondecreasing, box_ptr[K] = N (basis functions numbered box by box)
+ *   sig, B   complex64 [ndir][ncomp][Nz][Ny][Nx]: the layout fmmt_translate_multi uses
+ *   w        float [ndir]: quadrature weights
+ *   y        complex64 [N]
+ * Sharded contexts: each rank passes its own direction block (P, B, w rows); y is summed
+ * over ranks (ncclAllReduce).  FP32 accumulation.  Errors: FMMT_E_ARG (null or host
+ * pointer, ncomp out of range), FMMT_E_SHAPE (sizes), FMMT_E_STATE (wrong device),
+ * FMMT_E_NOMEM (workspace).  box_ptr contents are not validated (a malformed box_ptr is
+ * undefined behaviour).  Asynchronous on the context stream.                      */
+fmmt_status fmmt_aggregate(fmmt_ctx* ctx, const fmmt_c64* P, const fmmt_c64* I, const int64_t* box_ptr,
+                           int64_t ndir, int64_t N, int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz,
+                           fmmt_c64* sig);
+fmmt_status fmmt_disaggregate(fmmt_ctx* ctx, const fmmt_c64* P, const fmmt_c64* B, const float* w,
+                              const int64_t* box_ptr, int64_t ndir, int64_t N, int64_t ncomp, int64_t Nx,
+                              int64_t Ny, int64_t Nz, fmmt_c64* y);
+/* The far-field part of one matrix-vector product: eq. (4) -> eq. (5) with this op's
+ * compressed operators for every direction and component -> eq. (6), as one CUDA graph
+ * (workspaces owned by the op).  ndir and the grid must match the op.             */
+fmmt_status fmmt_far_matvec(fmmt_op* op, const fmmt_c64* P, const fmmt_c64* I, const int64_t* box_ptr,
+                            const float* w, int64_t ndir, int64_t N, int64_t ncomp, int64_t Nx, int64_t Ny,
+                            int64_t Nz, fmmt_c64* y);
+
 /* Test hook (not the hot path): restore T_p (local direction index p) from
  * the compressed form into the device buffer T_p (complex64 [n3][n2][n1])
  * with the same restore kernels and arithmetic the translate path uses.     */

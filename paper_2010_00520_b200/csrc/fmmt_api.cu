@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "fmmt_internal.h"
+#include "kernels_agg.cuh"
 #include "kernels_fft.cuh"
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
@@ -262,7 +263,7 @@ struct fmmt_op {
   int64_t partial_elems = 0;
   // CUDA graphs of whole matvecs, keyed by the buffers they read / write
   struct GraphEntry {
-    const void* key[5];
+    const void* key[6];
     int calls = 0;
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;   // kernels inside the graph
@@ -272,6 +273,9 @@ struct fmmt_op {
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
   float2* d_sum_host = nullptr;
+  // far-field matvec (fmmt_far_matvec): aggregated and translated signatures [ndir][ncomp][K]
+  float2 *fA = nullptr, *fB = nullptr, *fPart = nullptr;   // + disaggregation partials [nsplit][N]
+  int64_t fAB_elems = 0, fPart_elems = 0;
 };
 
 static int64_t rk(const fmmt_op* op, int64_t p, int slot) {
@@ -311,6 +315,9 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->d_in_host) cudaFree(op->d_in_host);
   if (op->d_w_host) cudaFree(op->d_w_host);
   if (op->d_sum_host) cudaFree(op->d_sum_host);
+  if (op->fA) cudaFree(op->fA);
+  if (op->fB) cudaFree(op->fB);
+  if (op->fPart) cudaFree(op->fPart);
   delete op;
 }
 
@@ -958,7 +965,7 @@ static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void*
 // on the legacy default stream (not capturable).
 template <class F>
 static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, const void* k2, const void* k3, int64_t k4,
-                               F&& body) {
+                               F&& body, const void* k5 = nullptr) {
   fmmt_ctx* ctx = op->ctx;
   if (ctx->stream == nullptr || !ctx->use_graphs) return body();
   if (ctx->profiling) {
@@ -983,7 +990,9 @@ static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, cons
   }
   fmmt_op::GraphEntry* ge = nullptr;
   for (auto& g : op->graphs)
-    if (g.key[0] == k0 && g.key[1] == k1 && g.key[2] == k2 && g.key[3] == k3 && g.key[4] == (const void*)k4) ge = &g;
+    if (g.key[0] == k0 && g.key[1] == k1 && g.key[2] == k2 && g.key[3] == k3 && g.key[4] == (const void*)k4 &&
+        g.key[5] == k5)
+      ge = &g;
   if (ge && ge->exec) {
     FMMT_CUDA(ctx, cudaGraphLaunch(ge->exec, ctx->stream));
     ctx->launches += ge->launches;
@@ -991,7 +1000,7 @@ static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, cons
   }
   if (!ge) {   // first call: run directly (allocates lazily sized workspaces), remember the key
     fmmt_op::GraphEntry e;
-    e.key[0] = k0; e.key[1] = k1; e.key[2] = k2; e.key[3] = k3; e.key[4] = (const void*)k4;
+    e.key[0] = k0; e.key[1] = k1; e.key[2] = k2; e.key[3] = k3; e.key[4] = (const void*)k4; e.key[5] = k5;
     e.calls = 1;
     op->graphs.push_back(e);
     return body();
@@ -1082,6 +1091,7 @@ void fmmt_destroy(fmmt_ctx* ctx) {
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
+  if (ctx->agg_part) cudaFree(ctx->agg_part);
   fmmt_internal::setup_release(ctx);
   delete ctx;
 }
@@ -1341,6 +1351,161 @@ fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, co
   FMMT_CUDA(ctx, cudaMemcpyAsync(sum_out_host, op->d_sum_host, K * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FMMT_OK;
+}
+
+// ---------------------------------------------------------------- aggregation / disaggregation
+static fmmt_status check_device_ptr(fmmt_ctx* ctx, const void* ptr, const char* what) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, FMMT_E_ARG, "%s is not a CUDA device pointer", what);
+  }
+  if (!(a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged))
+    return set_err(ctx, FMMT_E_ARG, "%s must be device memory", what);
+  if (a.type == cudaMemoryTypeDevice && a.device != ctx->device)
+    return set_err(ctx, FMMT_E_STATE, "%s is on device %d, context on %d", what, a.device, ctx->device);
+  return FMMT_OK;
+}
+
+static fmmt_status check_agg_args(fmmt_ctx* ctx, const void* P, const void* box_ptr, int64_t ndir, int64_t N,
+                                  int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz) {
+  CHECK_ARG(ctx, P && box_ptr, "null pointer");
+  CHECK_SHAPE(ctx, ndir >= 1 && N >= 0 && Nx >= 1 && Ny >= 1 && Nz >= 1, "bad sizes ndir %lld N %lld grid %lldx%lldx%lld",
+              (long long)ndir, (long long)N, (long long)Nx, (long long)Ny, (long long)Nz);
+  CHECK_ARG(ctx, ncomp >= 1 && ncomp <= 16, "ncomp %lld not in [1, 16]", (long long)ncomp);
+  fmmt_status st;
+  if ((st = check_device_ptr(ctx, box_ptr, "box_ptr"))) return st;
+  if (N > 0 && (st = check_device_ptr(ctx, P, "P"))) return st;
+  return FMMT_OK;
+}
+
+static fmmt_status aggregate_impl(fmmt_ctx* ctx, const float2* P, const float2* I, const int64_t* box_ptr, int64_t ndir,
+                                  int64_t N, int ncomp, int64_t K, float2* sig) {
+  ProfScope ps(ctx, "aggregate");
+  // a warp per (box, block of AGG_PD directions); the generic kernel: a warp per (box, direction)
+  const dim3 grid((unsigned)((K + 7) / 8), (unsigned)((ndir + fmmt::AGG_PD - 1) / fmmt::AGG_PD));
+  const dim3 grid_any((unsigned)((K + 7) / 8), (unsigned)std::min<int64_t>(ndir, 65535));
+  switch (ncomp) {
+    case 1: fmmt::k_aggregate<1><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
+    case 2: fmmt::k_aggregate<2><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
+    case 4: fmmt::k_aggregate<4><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
+    default: fmmt::k_aggregate_any<<<grid_any, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, ncomp, K, sig);
+  }
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+// direction blocks of the disaggregation: up to 16 (non-empty boxes x blocks fill the SMs; the partial
+// sums add 16 N complex writes + reads against the ndir N ncomp complex pattern reads)
+static int agg_nsplit(const fmmt_ctx*, int64_t ndir, int64_t) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(16, ndir / 16));   // >= 16 directions per block
+}
+
+// part: nsplit x N complex64 workspace
+static fmmt_status disaggregate_impl(fmmt_ctx* ctx, const float2* P, const float2* B, const float* w,
+                                     const int64_t* box_ptr, int64_t ndir, int64_t N, int ncomp, int64_t K, float2* y,
+                                     float2* part) {
+  if (N == 0) return FMMT_OK;
+  const int nsplit = agg_nsplit(ctx, ndir, K);
+  {
+    ProfScope ps(ctx, "disaggregate_partial");
+    const dim3 grid((unsigned)K, (unsigned)nsplit);
+    switch (ncomp) {
+      case 1: fmmt::k_disaggregate_partial<1><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;
+      case 2: fmmt::k_disaggregate_partial<2><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;
+      case 4: fmmt::k_disaggregate_partial<4><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;
+      default:
+        fmmt::k_disaggregate_partial_any<<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, ncomp, K, nsplit, part);
+    }
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  {
+    ProfScope ps(ctx, "disaggregate_final");
+    fmmt::k_disaggregate_final<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(part, N, nsplit, y);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  if (ctx->world > 1) {
+    ncclResult_t r = ncclAllReduce(y, y, (size_t)(2 * N), ncclFloat, ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream);
+    if (r != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+  }
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_aggregate(fmmt_ctx* ctx, const fmmt_c64* P, const fmmt_c64* I, const int64_t* box_ptr, int64_t ndir,
+                           int64_t N, int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz, fmmt_c64* sig) {
+  if (!ctx) return FMMT_E_ARG;
+  CHECK_ARG(ctx, sig && (I || N == 0), "null pointer");
+  fmmt_status st = check_agg_args(ctx, P ? P : (const void*)box_ptr, box_ptr, ndir, N, ncomp, Nx, Ny, Nz);
+  if (st) return st;
+  if ((st = check_device_ptr(ctx, sig, "sig"))) return st;
+  cudaSetDevice(ctx->device);
+  return aggregate_impl(ctx, reinterpret_cast<const float2*>(P), reinterpret_cast<const float2*>(I), box_ptr, ndir, N,
+                        (int)ncomp, Nx * Ny * Nz, reinterpret_cast<float2*>(sig));
+}
+
+fmmt_status fmmt_disaggregate(fmmt_ctx* ctx, const fmmt_c64* P, const fmmt_c64* B, const float* w, const int64_t* box_ptr,
+                              int64_t ndir, int64_t N, int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz, fmmt_c64* y) {
+  if (!ctx) return FMMT_E_ARG;
+  CHECK_ARG(ctx, B && w && (y || N == 0), "null pointer");
+  fmmt_status st = check_agg_args(ctx, P ? P : (const void*)box_ptr, box_ptr, ndir, N, ncomp, Nx, Ny, Nz);
+  if (st) return st;
+  if ((st = check_device_ptr(ctx, B, "B"))) return st;
+  cudaSetDevice(ctx->device);
+  const int64_t need = (int64_t)agg_nsplit(ctx, ndir, Nx * Ny * Nz) * N;
+  if (ctx->agg_part_elems < need) {
+    if (ctx->agg_part) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->agg_part);
+    }
+    ctx->agg_part = nullptr;
+    ctx->agg_part_elems = 0;
+    cudaError_t e = cudaMalloc(&ctx->agg_part, need * sizeof(float2));
+    if (e != cudaSuccess) return set_err(ctx, FMMT_E_NOMEM, "disaggregation workspace: %s", cudaGetErrorString(e));
+    ctx->agg_part_elems = need;
+  }
+  return disaggregate_impl(ctx, reinterpret_cast<const float2*>(P), reinterpret_cast<const float2*>(B), w, box_ptr, ndir,
+                           N, (int)ncomp, Nx * Ny * Nz, reinterpret_cast<float2*>(y),
+                           reinterpret_cast<float2*>(ctx->agg_part));
+}
+
+fmmt_status fmmt_far_matvec(fmmt_op* op, const fmmt_c64* P, const fmmt_c64* I, const int64_t* box_ptr, const float* w,
+                            int64_t ndir, int64_t N, int64_t ncomp, int64_t Nx, int64_t Ny, int64_t Nz, fmmt_c64* y) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, I && w && y, "null pointer");
+  fmmt_status st = check_agg_args(ctx, P, box_ptr, ndir, N, ncomp, Nx, Ny, Nz);
+  if (st) return st;
+  CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
+  CHECK_SHAPE(ctx, 2 * Nx == op->n1 && 2 * Ny == op->n2 && 2 * Nz == op->n3, "grid does not match the op");
+  cudaSetDevice(ctx->device);
+  const int64_t K = Nx * Ny * Nz, elems = ndir * ncomp * K;
+  const int64_t pelems = std::max<int64_t>(1, (int64_t)agg_nsplit(ctx, ndir, K) * N);
+  if (op->fAB_elems < elems || op->fPart_elems < pelems) {   // workspaces change: drop captured graphs
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& g : op->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    op->graphs.clear();
+    op->ws_bytes -= (2 * op->fAB_elems + op->fPart_elems) * 8;
+    for (float2** b : {&op->fA, &op->fB, &op->fPart})
+      if (*b) cudaFree(*b);
+    op->fA = op->fB = op->fPart = nullptr;
+    op->fAB_elems = op->fPart_elems = 0;
+    if ((st = cmalloc(op, &op->fA, elems)) || (st = cmalloc(op, &op->fB, elems)) || (st = cmalloc(op, &op->fPart, pelems)))
+      return st;
+    op->fAB_elems = elems;
+    op->fPart_elems = pelems;
+  }
+  if ((st = ensure_w(op, ncomp))) return st;
+  return run_graphed(op, P, I, y, w, N * 16 + ncomp, [&] {
+    fmmt_status s2 = aggregate_impl(ctx, reinterpret_cast<const float2*>(P), reinterpret_cast<const float2*>(I), box_ptr,
+                                    ndir, N, (int)ncomp, K, op->fA);
+    if (s2) return s2;
+    if ((s2 = translate_impl(op, reinterpret_cast<const fmmt_c64*>(op->fA), reinterpret_cast<fmmt_c64*>(op->fB),
+                             (int)ncomp)))
+      return s2;
+    return disaggregate_impl(ctx, reinterpret_cast<const float2*>(P), op->fB, w, box_ptr, ndir, N, (int)ncomp, K,
+                             reinterpret_cast<float2*>(y), op->fPart);
+  }, box_ptr);
 }
 
 fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {

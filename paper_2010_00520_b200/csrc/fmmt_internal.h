@@ -25,12 +25,14 @@ struct fmmt_ctx {
   int64_t launches = 0;
   bool profiling = false;
   int num_sms = 148;                // SM count of the device (persistent grids)
-  int gemm_impl = 1;
-  bool use_graphs = true;
-  bool z_multidir = false;
-  bool pack_factors = true;
-  int tc_ctas_per_sm = 4;
-  bool warp_specialised = false;    // tensor-core kernels: producer / consumer warps, 1 CTA/SM (FMMT_WS)           // tensor-core GEMM grid: CTAs per SM (each loops over tiles)         // keep pre-split copies of static slice-GEMM factors (2x their bytes)          // TT-4D z-stage: several directions per tile (1 CTA/SM; slower, A/B)           // replay whole matvecs as CUDA graphs (see run_graphed)                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA
+  int gemm_impl = 1;                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA, 2 = first tcgen05 design
+  bool use_graphs = true;           // replay whole matvecs as CUDA graphs (see run_graphed)
+  bool z_multidir = false;          // TT-4D z-stage: several directions per tile (1 CTA/SM; slower, A/B)
+  bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)
+  int tc_ctas_per_sm = 4;           // tensor-core GEMM grid: CTAs per SM (each loops over tiles)
+  bool warp_specialised = false;    // tensor-core kernels: producer / consumer warps, 1 CTA/SM (FMMT_WS)
+  void* agg_part = nullptr;         // disaggregation partial sums [nsplit][N] (complex64)
+  int64_t agg_part_elems = 0;
   std::vector<fmmt_prof_entry> pending;
   std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
   std::vector<cudaEvent_t> event_pool;

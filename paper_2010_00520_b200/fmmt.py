@@ -81,6 +81,9 @@ fmmt_restore = _sig("fmmt_restore", C.c_int, vp, i64, vp)
 fmmt_translate_multi = _sig("fmmt_translate_multi", C.c_int, vp, vp, vp, i64, i64, i64, i64, i64)
 fmmt_translate_sum_multi = _sig("fmmt_translate_sum_multi", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64)
 fmmt_set_gemm_impl = _sig("fmmt_set_gemm_impl", C.c_int, vp, C.c_int)
+fmmt_aggregate = _sig("fmmt_aggregate", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp)
+fmmt_disaggregate = _sig("fmmt_disaggregate", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp)
+fmmt_far_matvec = _sig("fmmt_far_matvec", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp)
 fmmt_test_cgemm = _sig("fmmt_test_cgemm", C.c_int, vp, C.c_int, i64, i64, i64, C.c_int, C.c_int, vp, i64, vp, i64, vp, i64)
 
 EXPORTED = [
@@ -90,6 +93,7 @@ EXPORTED = [
     "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_set_batch", "fmmt_translate",
     "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
     "fmmt_translate_multi", "fmmt_translate_sum_multi", "fmmt_build_operator_lossy",
+    "fmmt_aggregate", "fmmt_disaggregate", "fmmt_far_matvec",
 ]
 
 
@@ -215,6 +219,16 @@ class Context:
                self.h, "fmmt_compress")
         return Op(self, h)
 
+    def aggregate(self, P, I, box_ptr, ndir, N_basis, ncomp, N, sig):
+        """eq. (4): sig[p][c][Nz][Ny][Nx] from patterns P [ndir][N_basis][ncomp] and coefficients I."""
+        _check(fmmt_aggregate(self.h, _ptr(P), _ptr(I), _ptr(box_ptr), ndir, N_basis, ncomp, N[0], N[1], N[2],
+                              _ptr(sig)), self.h, "fmmt_aggregate")
+
+    def disaggregate(self, P, B, w, box_ptr, ndir, N_basis, ncomp, N, y):
+        """eq. (6): y[m] = sum_p w_p sum_c conj(P[p][m][c]) B[p][c][v(m)]."""
+        _check(fmmt_disaggregate(self.h, _ptr(P), _ptr(B), _ptr(w), _ptr(box_ptr), ndir, N_basis, ncomp,
+                                 N[0], N[1], N[2], _ptr(y)), self.h, "fmmt_disaggregate")
+
     def import_op(self, fmt, n, ndir, ranks, arrays) -> "Op":
         """arrays: list of complex64 numpy arrays (flattened in library layout)."""
         fmt = FORMATS[fmt] if isinstance(fmt, str) else fmt
@@ -283,6 +297,11 @@ class Op:
     def translate_sum_multi(self, sig_in, sig_out, w, sum_out, ndir, ncomp, N):
         _check(fmmt_translate_sum_multi(self.h, _ptr(sig_in), _ptr(sig_out), _ptr(w), _ptr(sum_out), ndir, ncomp,
                                         N[0], N[1], N[2]), self.ctx.h, "fmmt_translate_sum_multi")
+
+    def far_matvec(self, P, I, box_ptr, w, ndir, N_basis, ncomp, N, y):
+        """eq. (4) -> eq. (5) with this op -> eq. (6), one graph."""
+        _check(fmmt_far_matvec(self.h, _ptr(P), _ptr(I), _ptr(box_ptr), _ptr(w), ndir, N_basis, ncomp,
+                               N[0], N[1], N[2], _ptr(y)), self.ctx.h, "fmmt_far_matvec")
 
     def restore(self, p: int, out):
         _check(fmmt_restore(self.h, p, _ptr(out)), self.ctx.h, "fmmt_restore")

@@ -1,0 +1,5 @@
+set -x
+cd $GRAFT_REPO_ROOT
+export PYTHONPATH=.
+timeout 300 python scripts/agg_probe.py 2 20 > gpurun_out/agg_probe.txt 2>&1; echo "probe exit $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_aggregate|k_disaggregate_partial' -c 2 -o gpurun_out/prof_agg python scripts/agg_probe.py 2 1 > gpurun_out/ncu_agg.log 2>&1; echo "ncu exit $?"
