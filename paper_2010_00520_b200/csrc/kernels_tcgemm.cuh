@@ -130,7 +130,15 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   const uint32_t twarp = tmem + ((uint32_t)(wrow * 32) << 16);   // this warp's TMEM lanes
   const int c0 = grp * NRG;                                      // this group's columns
 
-  const int nk = (d.k + BK - 1) / BK;
+  // warp-uniform copies (the MMA-issuing warp 0 keeps its operands in uniform registers)
+  const int nk = __shfl_sync(0xffffffffu, (d.k + BK - 1) / BK, 0);
+  const int cur_c = __shfl_sync(0xffffffffu, cur.c, 0), cur_g = __shfl_sync(0xffffffffu, cur.g, 0);
+  const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const uint32_t sbase_u = __shfl_sync(0xffffffffu, sbase, 0);
+  const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+  const uint32_t bar_u = __shfl_sync(0xffffffffu, tc::smem_u32(bar), 0);
+  const uint64_t dAh = tc::sdesc(sbase_u, Cfg::LBO_A, 128), dAl = tc::sdesc(sbase_u + Cfg::A_BYTES, Cfg::LBO_A, 128);
+  const uint64_t dBp = tc::sdesc(sbase_u + 2 * Cfg::A_BYTES, Cfg::LBO_B, 128);
   const bool apack = d.Ap != nullptr;   // A pre-split into hi/lo tiles: one bulk copy per chunk
   const float* apk = apack ? d.Ap + (int64_t)(m0 / BM) * d.a_nkc * TC_PACK_FLOATS : nullptr;
   // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
@@ -278,24 +286,25 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     }
     tc::fence_async_smem();
     tc::mbar_arrive(&full[s]);
-    if (tid == 0) {
-      tc::mbar_wait(&full[s], ph);                    // all 128 threads' operands of chunk kc are in place
-      const int g = cur.g + kc / TC_FC;               // CTA-wide flush group (TMEM slot, tfree phase)
+    if (warp_u == 0) {                                // warp 0 issues; one elected lane per tcgen05 op
+      __syncwarp();
+      const int gcu = cur_c + kc;
+      const int su = gcu % TC_NS;
+      tc::mbar_wait_addr(bar_u + (2 * TC_NS + su) * 8, (gcu / TC_NS) & 1);   // chunk kc's operands in place
+      const int g = cur_g + kc / TC_FC;               // CTA-wide flush group (TMEM slot, tfree phase)
       const bool fresh = kc % TC_FC == 0;             // first chunk of a flush group
-      if (fresh && g >= 2) tc::mbar_wait(&tfree[g & 1], ((g >> 1) - 1) & 1);   // group g-2 drained
+      if (fresh && g >= 2) tc::mbar_wait_addr(bar_u + (3 * TC_NS + (g & 1)) * 8, ((g >> 1) - 1) & 1);   // g-2 drained
+      __syncwarp();
       tc::fence_after_sync();
-      const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
-      const uint32_t sb = sa_hi + 2 * Cfg::A_BYTES;
-      const uint32_t tm = tmem + (g & 1) * 2 * NR, tx = tm + NR;
+      const uint64_t so = (uint64_t)((su * Cfg::STAGE) >> 4);   // descriptor start-address units
+      const uint32_t tm = tmem_u + (g & 1) * 2 * NR, tx = tm + NR;
 #pragma unroll
       for (int ks = 0; ks < Cfg::KR / 8; ++ks) {
-        const uint64_t ah = tc::sdesc(sa_hi + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
-        const uint64_t al = tc::sdesc(sa_lo + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
-        const uint64_t bp = tc::sdesc(sb + ks * 2 * Cfg::LBO_B, Cfg::LBO_B, 128);   // rows [0, 2NR)
-        tc::mma_tf32(tm, ah, bp, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
-        tc::mma_tf32(tx, al, bp, IDESC_B, 1);                       // += lo.hi  (rows [0, NR) of B')
+        const uint64_t oa = so + ((ks * 2 * Cfg::LBO_A) >> 4), ob = so + ((ks * 2 * Cfg::LBO_B) >> 4);
+        tc::mma_tf32_el(tm, dAh + oa, dBp + ob, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
+        tc::mma_tf32_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);                       // += lo.hi (rows [0, NR))
       }
-      tc::mma_commit(&mmab[s]);
+      tc::mma_commit_el(bar_u + su * 8);              // -> mmab[su]
     }
   }
   tc::cp_async_wait<0>();
