@@ -69,7 +69,14 @@ __device__ __forceinline__ void tcw_produce(const GemmDesc& d, const float2* __r
   }
   constexpr uint32_t IDESC_BP = tc::idesc_tf32(BM, 2 * NR);
   constexpr uint32_t IDESC_B = tc::idesc_tf32(BM, NR);
-  const int nk = (d.k + BK - 1) / BK;
+  const int nk = __shfl_sync(0xffffffffu, (d.k + BK - 1) / BK, 0);   // warp-uniform (see tc_mainloop)
+  const int cur_c = __shfl_sync(0xffffffffu, cur.c, 0), cur_g = __shfl_sync(0xffffffffu, cur.g, 0);
+  const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const uint32_t sbase_u = __shfl_sync(0xffffffffu, sbase, 0);
+  const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+  const uint32_t bar_u = __shfl_sync(0xffffffffu, tc::smem_u32(bar), 0);
+  const uint64_t dAh = tc::sdesc(sbase_u, Cfg::LBO_A, 128), dAl = tc::sdesc(sbase_u + Cfg::A_BYTES, Cfg::LBO_A, 128);
+  const uint64_t dBp = tc::sdesc(sbase_u + 2 * Cfg::A_BYTES, Cfg::LBO_B, 128);
   const bool apack = d.Ap != nullptr;
   const float* apk = apack ? d.Ap + (int64_t)(m0 / BM) * d.a_nkc * TC_PACK_FLOATS : nullptr;
 
@@ -178,25 +185,26 @@ __device__ __forceinline__ void tcw_produce(const GemmDesc& d, const float2* __r
     }
     tc::fence_async_smem();
     tc::mbar_arrive(&full[s]);
-    if (tid == 0) {
-      tc::mbar_wait(&full[s], ph);
-      const int g = cur.g + kc / TC_FC;
+    if (warp_u == 0) {                                // warp 0 issues (elect.sync per tcgen05 op)
+      __syncwarp();
+      const int gcu = cur_c + kc;
+      const int su = gcu % NS;
+      tc::mbar_wait_addr(bar_u + (2 * NS + su) * 8, (gcu / NS) & 1);           // full[su]
+      const int g = cur_g + kc / TC_FC;
       const bool fresh = kc % TC_FC == 0;
-      if (fresh && g >= 2) tc::mbar_wait(&tfree[g & 1], ((g >> 1) - 1) & 1);
+      if (fresh && g >= 2) tc::mbar_wait_addr(bar_u + (3 * NS + 2 + (g & 1)) * 8, ((g >> 1) - 1) & 1);   // tfree
+      __syncwarp();
       tc::fence_after_sync();
-      const uint32_t sa_hi = sbase + s * Cfg::STAGE, sa_lo = sa_hi + Cfg::A_BYTES;
-      const uint32_t sb = sa_hi + 2 * Cfg::A_BYTES;
-      const uint32_t tm = tmem + (g & 1) * 2 * NR, tx = tm + NR;
+      const uint64_t so = (uint64_t)((su * Cfg::STAGE) >> 4);
+      const uint32_t tm = tmem_u + (g & 1) * 2 * NR, tx = tm + NR;
 #pragma unroll
       for (int ks = 0; ks < Cfg::KR / 8; ++ks) {
-        const uint64_t ah = tc::sdesc(sa_hi + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
-        const uint64_t al = tc::sdesc(sa_lo + ks * 2 * Cfg::LBO_A, Cfg::LBO_A, 128);
-        const uint64_t bp = tc::sdesc(sb + ks * 2 * Cfg::LBO_B, Cfg::LBO_B, 128);
-        tc::mma_tf32(tm, ah, bp, IDESC_BP, !(fresh && ks == 0));
-        tc::mma_tf32(tx, al, bp, IDESC_B, 1);
+        const uint64_t oa = so + ((ks * 2 * Cfg::LBO_A) >> 4), ob = so + ((ks * 2 * Cfg::LBO_B) >> 4);
+        tc::mma_tf32_el(tm, dAh + oa, dBp + ob, IDESC_BP, !(fresh && ks == 0));
+        tc::mma_tf32_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);
       }
-      tc::mma_commit(&mmab[s]);
-      if (kc % TC_FC == TC_FC - 1 || kc == nk - 1) tc::mma_commit(&tfull[g & 1]);   // group complete
+      tc::mma_commit_el(bar_u + su * 8);                                        // mmab[su]
+      if (kc % TC_FC == TC_FC - 1 || kc == nk - 1) tc::mma_commit_el(bar_u + (3 * NS + (g & 1)) * 8);   // tfull
     }
   }
   tc::cp_async_wait<0>();
