@@ -274,6 +274,8 @@ struct fmmt_op {
   float* d_w_host = nullptr;
   float2* d_sum_host = nullptr;
   // far-field matvec (fmmt_far_matvec): aggregated and translated signatures [ndir][ncomp][K]
+  float* Vpk = nullptr;                         // TT-4D z-stage: pre-split V_q of a batch (k_tc_pack_b)
+  int64_t vpk_floats = 0;
   float2 *fA = nullptr, *fB = nullptr, *fPart = nullptr;   // + disaggregation partials [nsplit][N]
   int64_t fAB_elems = 0, fPart_elems = 0;
 };
@@ -318,6 +320,7 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->fA) cudaFree(op->fA);
   if (op->fB) cudaFree(op->fB);
   if (op->fPart) cudaFree(op->fPart);
+  if (op->Vpk) cudaFree(op->Vpk);
   delete op;
 }
 
@@ -731,6 +734,37 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
   }
 }
 
+// k_tc_pack_b of the z-stage's V_q (batch of nq directions) into op->Vpk; sets a.Vp / a.vp_stride.
+template <int BN>
+static fmmt_status pack_v_bn(fmmt_op* op, ZArgs& a, int nq) {
+  fmmt_ctx* ctx = op->ctx;
+  using Cfg = fmmt::TcGemmCfg<BN, 1>;
+  const int k = a.rank, n = (int)op->n3;
+  const int64_t nkc = (k + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (n + BN - 1) / BN;
+  const int64_t per_q = tiles_n * nkc * Cfg::BP_FLOATS;
+  const int64_t need = per_q * nq;
+  if (op->vpk_floats < need)   // allocated by ensure_w (outside any graph capture) for the largest batch
+    return set_err(ctx, FMMT_E_STATE, "pre-split V workspace too small (%lld < %lld floats)",
+                   (long long)op->vpk_floats, (long long)need);
+  {
+    ProfScope ps(ctx, "pack_v");
+    const int64_t items = need / Cfg::BP_FLOATS * BN * (fmmt::TC_BK / 2);
+    const unsigned grid = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
+    fmmt::k_tc_pack_b<BN><<<grid, 256, 0, ctx->stream>>>(a.V, a.v_stride, a.v_sc, a.v_sk, k, n, nq, op->Vpk);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  a.Vp = op->Vpk;
+  a.vp_stride = per_q;
+  return FMMT_OK;
+}
+
+static fmmt_status pack_v(fmmt_op* op, ZArgs& a, int nq) {
+  switch (op->n3) {
+    case 4: case 8: case 16: return pack_v_bn<16>(op, a, nq);
+    default: return pack_v_bn<32>(op, a, nq);
+  }
+}
+
 template <int N3, int ND>
 static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
   constexpr int BN = N3 * ND < 16 ? 16 : N3 * ND;
@@ -833,6 +867,13 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     a.G = a.G + (int64_t)qoff * a.g_stride;
     if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
     a.Tout = Tout;
+    // TT-4D: A (T1) is pre-split once per op; pre-split this batch's V_q too, so the z-stage streams
+    // both operands with bulk copies and no per-thread conversion (FMMT_PACKB=0 disables)
+    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b && ctx->gemm_impl == 1 && !ctx->warp_specialised &&
+        !ctx->z_multidir) {
+      fmmt_status st = pack_v(op, a, nq);
+      if (st) return st;
+    }
     static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
                                    "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
@@ -892,8 +933,36 @@ static fmmt_status ensure_zscr(fmmt_op* op) {
   return st;
 }
 
+// TT-4D z-stage pre-split V_q workspace (pack_v) for the largest batch.
+static fmmt_status ensure_vpk(fmmt_op* op) {
+  fmmt_ctx* ctx = op->ctx;
+  if (op->format != FMMT_TT4D || !ctx->pack_b || op->n3 > 32) return FMMT_OK;
+  int64_t nq = 1;
+  for (const Batch& b : op->batches) nq = std::max<int64_t>(nq, b.nq);
+  const int BN = op->n3 <= 16 ? 16 : 32;
+  const int64_t nkc = (rk(op, 0, 1) + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (op->n3 + BN - 1) / BN;
+  const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK);   // BP_FLOATS = 2 NR x 2 BK, NR = 2 BN
+  if (op->vpk_floats >= need) return FMMT_OK;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& g : op->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  op->graphs.clear();
+  if (op->Vpk) {
+    cudaFree(op->Vpk);
+    op->ws_bytes -= op->vpk_floats * 4;
+  }
+  op->Vpk = nullptr;
+  op->vpk_floats = 0;
+  cudaError_t e = cudaMalloc(&op->Vpk, need * sizeof(float));
+  if (e != cudaSuccess) return set_err(ctx, FMMT_E_NOMEM, "pre-split V workspace: %s", cudaGetErrorString(e));
+  op->vpk_floats = need;
+  op->ws_bytes += need * 4;
+  return FMMT_OK;
+}
+
 // W (the half-padded spectra of every direction and component) sized for ncomp components.
 static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
+  if (fmmt_status st = ensure_vpk(op)) return st;
   if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
   fmmt_ctx* ctx = op->ctx;
   cudaStreamSynchronize(ctx->stream);
@@ -1063,6 +1132,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
   if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_PACKB")) ctx->pack_b = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_WS")) ctx->warp_specialised = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -1520,6 +1590,7 @@ fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
     FMMT_CUDA(ctx, cudaMemcpyAsync(T_p, op->arr[0] + p * n, n * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
     return FMMT_OK;
   }
+  if (fmmt_status st = ensure_vpk(op)) return st;
   for (const Batch& b : op->batches) {
     if (p < b.q0 || p >= b.q0 + b.nq) continue;
     fmmt_status st = run_batch_prep(op, b);

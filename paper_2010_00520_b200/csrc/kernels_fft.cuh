@@ -316,6 +316,8 @@ struct ZArgs {
   int64_t v_sc, v_sk;        // element (c, k) at V + off + c*v_sc + k*v_sk
   const int* rank_p;         // per op direction, or nullptr
   int rank;                  // uniform rank when rank_p == nullptr
+  const float* Vp;           // V pre-split for the tensor-core kernel (k_tc_pack_b), or nullptr
+  int64_t vp_stride;         // floats per batch-local q
   // dense operator: T[p][k][ij]
   const float2* T;
   // restore output [k][ij]

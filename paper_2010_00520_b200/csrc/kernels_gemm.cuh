@@ -33,6 +33,9 @@ struct GemmDesc {
   const float* Ap;
   int a_nkc;
   int b_eo;            // tensor-core z-stage: B columns taken in (even, odd) order
+  // optional pre-split B (k_tc_pack_b) of this tile's columns: chunk c at Bp + c * TcGemmCfg::BP_FLOATS
+  // (set per tile by the kernel); nullptr = none
+  const float* Bp;
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {

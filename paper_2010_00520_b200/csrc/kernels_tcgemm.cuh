@@ -49,6 +49,7 @@ struct TcGemmCfg {
   static constexpr int A_BYTES = TC_BM * KR * 4;    // one of hi / lo (16 KB)
   static constexpr int BP_ROWS = 2 * NR;            // B' = [B^_hi ; B^_lo]
   static constexpr int BP_BYTES = BP_ROWS * KR * 4;
+  static constexpr int BP_FLOATS = BP_BYTES / 4;      // one pre-split B' chunk (k_tc_pack_b)
   static constexpr int BITEMS = BN * (TC_BK / 2) / NT > 0 ? BN * (TC_BK / 2) / NT : 1;
   static constexpr int BRAW = BITEMS * NT * 16;     // raw B staging
   static constexpr int STAGE = 2 * A_BYTES + BP_BYTES + BRAW;
@@ -140,17 +141,21 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   const uint64_t dAh = tc::sdesc(sbase_u, Cfg::LBO_A, 128), dAl = tc::sdesc(sbase_u + Cfg::A_BYTES, Cfg::LBO_A, 128);
   const uint64_t dBp = tc::sdesc(sbase_u + 2 * Cfg::A_BYTES, Cfg::LBO_B, 128);
   const bool apack = d.Ap != nullptr;   // A pre-split into hi/lo tiles: one bulk copy per chunk
+  const bool bpack = d.Bp != nullptr;   // B pre-split into B' chunks: one bulk copy per chunk
+  const bool both_u = __shfl_sync(0xffffffffu, (int)(apack && bpack), 0);   // no per-thread operand work
   const float* apk = apack ? d.Ap + (int64_t)(m0 / BM) * d.a_nkc * TC_PACK_FLOATS : nullptr;
   // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
   auto issue = [&](int c) {
     const int k0 = c * BK;
     const int cs = (cur.c + c) % TC_NS;
     const uint32_t st = sbase + cs * Cfg::STAGE;
+    if ((apack || bpack) && tid == 0) {   // pre-split operands: bulk async copies on one transaction barrier
+      tc::mbar_expect_tx(&bar[TC_NS + cs], (apack ? 2 * Cfg::A_BYTES : 0) + (bpack ? Cfg::BP_BYTES : 0));
+      if (apack) tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[TC_NS + cs]);
+      if (bpack)
+        tc::bulk_g2s(st + 2 * Cfg::A_BYTES, d.Bp + (int64_t)c * Cfg::BP_FLOATS, Cfg::BP_BYTES, &bar[TC_NS + cs]);
+    }
     if (apack) {
-      if (tid == 0) {
-        tc::mbar_expect_tx(&bar[TC_NS + cs], 2 * Cfg::A_BYTES);
-        tc::bulk_g2s(st, apk + (int64_t)c * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, &bar[TC_NS + cs]);
-      }
     } else if (!a_kcontig) {
       // row-per-thread: group g copies K elements [g BK/G, (g+1) BK/G) of its row
 #pragma unroll
@@ -181,6 +186,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     const uint32_t rb = st + 2 * Cfg::A_BYTES + Cfg::BP_BYTES;
 #pragma unroll
     for (int i = 0; i < BITEMS; ++i) {
+      if (bpack) break;
       const int idx = tid + NT * i;
       int j, kp;
       if (!b_kcontig) { j = idx % BN; kp = idx / BN; }    // n (not k) contiguous in memory
@@ -237,7 +243,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     if (kc + D < nk) issue(kc + D);
     else tc::cp_async_commit();          // keep one group per iteration
     tc::cp_async_wait<D>();              // this thread's copies of chunk kc have landed
-    if (apack) tc::mbar_wait(&abar[s], ph);
+    if (apack || bpack) tc::mbar_wait(&abar[s], ph);
     uint8_t* st = tcsm + s * Cfg::STAGE;
     uint8_t* aHi = st;
     uint8_t* aLo = st + Cfg::A_BYTES;
@@ -266,7 +272,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
 #pragma unroll
     for (int i = 0; i < BITEMS; ++i) {
       const int idx = tid + NT * i;
-      if (idx >= BN * (BK / 2)) continue;
+      if (bpack || idx >= BN * (BK / 2)) continue;
       int j, kp;
       if (!b_kcontig) { j = idx % BN; kp = idx / BN; }
       else { kp = idx % (BK / 2); j = idx / (BK / 2); }
@@ -284,7 +290,10 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       *reinterpret_cast<float4*>(bP + off + NR * 16) = l0;
       *reinterpret_cast<float4*>(bP + off + NR * 16 + 16) = l1;
     }
-    tc::fence_async_smem();
+    if (!both_u) tc::fence_async_smem();              // this thread's converted operands -> async proxy
+    // every thread arrives, also with two pre-split operands (nothing converted): the full[] barrier
+    // keeps warp 0 from running more than one chunk ahead of the slowest warp, which the abar /
+    // mmab parity waits need (a lead of NS chunks would alias their phases)
     tc::mbar_arrive(&full[s]);
     if (warp_u == 0) {                                // warp 0 issues; one elected lane per tcgen05 op
       __syncwarp();
@@ -436,6 +445,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
     d.sA = d.sB = d.sC = 0;
     d.Ap = a.Gp;                          // pre-split shared G (TT-4D T1), or nullptr
     d.a_nkc = (d.k + TC_BK - 1) / TC_BK;
+    d.Bp = (ND == 1 && a.Vp) ? a.Vp + (int64_t)q0 * a.vp_stride : nullptr;   // pre-split V_q, or nullptr
     const float2* A = a.G + (int64_t)q0 * a.g_stride;
     const float2* B = a.V + (a.v_off ? a.v_off[p0] : (int64_t)q0 * a.v_stride);
     const int64_t ij = m0 + row;
@@ -509,6 +519,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
   d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
   d.sA = d.sB = d.sC = 0;
   d.Ap = a.Gp;
+  d.Bp = nullptr;
   d.a_nkc = (d.k + TC_BK - 1) / TC_BK;
   const float2* A = a.G + (int64_t)q * a.g_stride;
   const float2* B = a.V + (a.v_off ? a.v_off[p] : (int64_t)q * a.v_stride);
@@ -596,6 +607,50 @@ __global__ void k_tc_pack_a(GemmDesc d, float* __restrict__ out) {
     const int off = r * 4 + kp * (TC_BM * 4);             // floats: row r -> 16 B, K core matrix -> TC_BM*16 B
     *reinterpret_cast<float4*>(tile + off) = hi;
     *reinterpret_cast<float4*>(tile + TC_PACK_FLOATS / 2 + off) = lo;
+  }
+}
+
+// ---------------------------------------------------------------- k_tc_pack_b
+// Pre-split B operands (one per batch-local q, columns [0, n)) into the B' chunks the tensor-core
+// mainloop would build in shared memory: per (q, n-tile, 8-complex K-chunk) one contiguous block of
+// BP_FLOATS = [B^_hi ; B^_lo] rows in the canonical K-major UMMA layout (rows 2j = [Re b, -Im b],
+// 2j+1 = [Im b, Re b], rna TF32 split), zero outside k x n.  The GEMM then streams B with one bulk
+// async copy per chunk.  B(l, j) of batch q at B + q * b_stride + l * b_sk + j * b_sn.
+template <int BN>
+__global__ void k_tc_pack_b(const float2* __restrict__ B, int64_t b_stride, int64_t b_sk, int64_t b_sn, int k, int n,
+                            int nq, float* __restrict__ out) {
+  using Cfg = TcGemmCfg<BN, 1>;
+  constexpr int NR = Cfg::NR;
+  const int nkc = (k + TC_BK - 1) / TC_BK;
+  const int tiles_n = (n + BN - 1) / BN;
+  const int64_t total = (int64_t)nq * tiles_n * nkc * BN * (TC_BK / 2);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % BN);                 // column in tile (fastest)
+    int64_t t = e / BN;
+    const int kp = (int)(t % (TC_BK / 2));
+    t /= (TC_BK / 2);
+    const int kc = (int)(t % nkc);
+    t /= nkc;
+    const int tn = (int)(t % tiles_n);
+    const int64_t q = t / tiles_n;
+    const int gn = tn * BN + j, gk = kc * TC_BK + 2 * kp;
+    float2 b0 = make_float2(0.f, 0.f), b1 = make_float2(0.f, 0.f);
+    if (gn < n) {
+      const float2* Bq = B + q * b_stride + (int64_t)gn * b_sn;
+      if (gk < k) b0 = Bq[(int64_t)gk * b_sk];
+      if (gk + 1 < k) b1 = Bq[(int64_t)(gk + 1) * b_sk];
+    }
+    float4 h0, l0, h1, l1;
+    tc::split_tf32(b0.x, h0.x, l0.x); tc::split_tf32(-b0.y, h0.y, l0.y);
+    tc::split_tf32(b1.x, h0.z, l0.z); tc::split_tf32(-b1.y, h0.w, l0.w);
+    tc::split_tf32(b0.y, h1.x, l1.x); tc::split_tf32(b0.x, h1.y, l1.y);
+    tc::split_tf32(b1.y, h1.z, l1.z); tc::split_tf32(b1.x, h1.w, l1.w);
+    float* blk = out + ((q * tiles_n + tn) * nkc + kc) * Cfg::BP_FLOATS;
+    const int off = (2 * j) * 4 + kp * (Cfg::LBO_B / 4);   // floats (the shared-memory B' layout)
+    *reinterpret_cast<float4*>(blk + off) = h0;
+    *reinterpret_cast<float4*>(blk + off + 4) = h1;
+    *reinterpret_cast<float4*>(blk + off + NR * 4) = l0;
+    *reinterpret_cast<float4*>(blk + off + NR * 4 + 4) = l1;
   }
 }
 

@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(256, 1) k_tcw_conv_z(ZArgs a, int nq) {
       d.c_s0 = 0; d.c_s1 = 0; d.c_div = 1; d.c_sn = 0;
       d.sA = d.sB = d.sC = 0;
       d.Ap = a.Gp;
+      d.Bp = nullptr;
       d.a_nkc = (rk + TC_BK - 1) / TC_BK;
       const float2* A = a.G + (int64_t)q * a.g_stride;
       const float2* B = a.V + (a.v_off ? a.v_off[p] : (int64_t)q * a.v_stride);
