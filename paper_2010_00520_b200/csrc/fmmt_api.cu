@@ -222,6 +222,8 @@ struct GemmLaunch {
   int tc_bn = 64;      // tensor-core kernel: complex columns per tile
   int tc_maxtiles = 0; // tensor-core kernel: tiles of 128 x tc_bn
   const char* name = "";
+  // pre-split the (dynamic) B operand of descriptor `first` into pack_dst before the launch
+  float* pack_dst = nullptr;
 };
 
 struct Batch {
@@ -274,6 +276,9 @@ struct fmmt_op {
   float* d_w_host = nullptr;
   float2* d_sum_host = nullptr;
   // far-field matvec (fmmt_far_matvec): aggregated and translated signatures [ndir][ncomp][K]
+  std::vector<float*> bpk_static;               // pre-split static B operands of the slice GEMMs (per batch)
+  float* Mpk = nullptr;                         // H-Tucker G GEMM: pre-split M_q of a batch
+  int64_t mpk_floats = 0;
   float* Vpk = nullptr;                         // TT-4D z-stage: pre-split V_q of a batch (k_tc_pack_b)
   int64_t vpk_floats = 0;
   float2 *fA = nullptr, *fB = nullptr, *fPart = nullptr;   // + disaggregation partials [nsplit][N]
@@ -321,6 +326,9 @@ void fmmt_op_destroy(fmmt_op* op) {
   if (op->fB) cudaFree(op->fB);
   if (op->fPart) cudaFree(op->fPart);
   if (op->Vpk) cudaFree(op->Vpk);
+  if (op->Mpk) cudaFree(op->Mpk);
+  for (auto b : op->bpk_static)
+    if (b) cudaFree(b);
   delete op;
 }
 
@@ -462,6 +470,46 @@ static fmmt_status with_packed_a(fmmt_op* op, int ai, GemmDesc& d) {
   return FMMT_OK;
 }
 
+// Pre-split B of a tensor-core descriptor (k_tc_pack_b with the launch's BN): floats needed and the launch.
+static int tc_bn_for(int64_t n) { return n >= 32 ? 32 : 16; }   // as add_gemm picks it (single-descriptor groups)
+
+static int64_t packb_floats(const GemmDesc& d) {
+  const int bn = tc_bn_for(d.n);
+  const int64_t nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (d.n + bn - 1) / bn;
+  return (int64_t)d.batch * tiles_n * nkc * (64 * bn);   // BP_FLOATS = 64 BN
+}
+
+static fmmt_status launch_pack_b(fmmt_ctx* ctx, const GemmDesc& d, float* out) {
+  const int bn = tc_bn_for(d.n);
+  const int64_t items = packb_floats(d) / (64 * bn) * bn * (fmmt::TC_BK / 2);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16));
+  ProfScope ps(ctx, "pack_b");
+  if (bn == 32)
+    fmmt::k_tc_pack_b<32><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out);
+  else
+    fmmt::k_tc_pack_b<16><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+// A descriptor whose B operand is static (factor rows of this batch): pre-split it once per op (synchronous).
+static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
+  fmmt_ctx* ctx = op->ctx;
+  if (!ctx->pack_b || ctx->gemm_impl != 1 || ctx->warp_specialised || !d.Ap) return FMMT_OK;
+  float* buf = nullptr;
+  const int64_t floats = packb_floats(d);
+  if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, FMMT_E_NOMEM, "pre-split B allocation (%lld B) failed", (long long)(floats * 4));
+  }
+  op->pack_bytes += floats * 4;
+  op->bpk_static.push_back(buf);
+  if (fmmt_status st = launch_pack_b(ctx, d, buf)) return st;
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  d.Bp = buf;
+  return FMMT_OK;
+}
+
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
 static void tucker_chain(fmmt_op* op, Batch& b) {
@@ -502,6 +550,12 @@ static fmmt_status build_plans(fmmt_op* op) {
   free_workspace(op);
   op->descs.clear();
   op->batches.clear();
+  for (auto b : op->bpk_static)
+    if (b) cudaFree(b);
+  op->bpk_static.clear();
+  if (op->Mpk) cudaFree(op->Mpk);
+  op->Mpk = nullptr;
+  op->mpk_floats = 0;
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
   if (op->PB <= 0) {
     const int64_t target = 48ll << 20;
@@ -547,6 +601,7 @@ static fmmt_status build_plans(fmmt_op* op) {
         // a3 (Fig. 3(b)): C_q = C(r1 r2 r3 x r4) . U4[p,:]^T
         GemmDesc ds = gd(op->arr[0], op->arr[4] + b.q0, op->Cw, r1 * r2 * r3, b.nq, r4, 1, r1 * r2 * r3, op->ndir, r1 * r2 * r3);
         if ((st = with_packed_a(op, 0, ds))) return st;
+        if ((st = with_packed_b_static(op, ds))) return st;
         add_gemm(op, b, {ds}, "slice_tucker4d");
         tucker_chain(op, b);
         break;
@@ -561,11 +616,30 @@ static fmmt_status build_plans(fmmt_op* op) {
         const float2 *U4 = op->arr[3], *C34 = op->arr[5];
         GemmDesc dm = gdx(C34, U4 + b.q0, op->Mw, r3 * r34, nq, r4, 1, r3 * r4, r3, r3, op->ndir, 1, 1, r3 * nq, r3, r3);
         if ((st = with_packed_a(op, 5, dm))) return st;
+        if ((st = with_packed_b_static(op, dm))) return st;
         add_gemm(op, b, {dm}, "slice_htucker_M");
         GemmDesc dg = gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12);
         dg.Ap = op->E_pk;
         dg.a_nkc = (int)((r34 + fmmt::TC_BK - 1) / fmmt::TC_BK);
+        float* mpk = nullptr;
+        if (dg.Ap && op->ctx->pack_b && op->ctx->gemm_impl == 1 && !op->ctx->warp_specialised) {
+          // M_q changes every batch: pre-split it into Mpk right before the G GEMM (sized for the largest batch)
+          const int64_t need = packb_floats(dg);
+          if (op->mpk_floats < need) {
+            if (op->Mpk) cudaFree(op->Mpk);
+            op->Mpk = nullptr;
+            op->mpk_floats = 0;
+            if (cudaMalloc(&op->Mpk, need * sizeof(float)) != cudaSuccess) {
+              cudaGetLastError();
+              return set_err(op->ctx, FMMT_E_NOMEM, "pre-split M allocation (%lld B) failed", (long long)(need * 4));
+            }
+            op->mpk_floats = need;
+          }
+          mpk = op->Mpk;
+          dg.Bp = mpk;
+        }
         add_gemm(op, b, {dg}, "slice_htucker_G");
+        b.gemms.back().pack_dst = mpk;
         break;
       }
       case FMMT_TT3D: {
@@ -586,6 +660,7 @@ static fmmt_status build_plans(fmmt_op* op) {
         // a3 (Fig. 4(b) step 1, columns of T2 for the batch): V_q = C2(r2 n3 x r3) . U_last[p,:]^T
         GemmDesc dv = gd(op->arr[2], op->arr[3] + b.q0, op->Vw, r2 * n3, b.nq, r3, 1, r2 * n3, op->ndir, r2 * n3);
         if ((st = with_packed_a(op, 2, dv))) return st;
+        if ((st = with_packed_b_static(op, dv))) return st;
         add_gemm(op, b, {dv}, "slice_tt4d");
         break;
       }
@@ -912,6 +987,8 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
 
 static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
   for (auto& L : b.gemms) {
+    if (L.pack_dst)   // the descriptor's B was produced by the previous launch: pre-split it now
+      if (fmmt_status st = launch_pack_b(op->ctx, op->descs[L.first], L.pack_dst)) return st;
     fmmt_status st = launch_gemm(op, L);
     if (st) return st;
   }

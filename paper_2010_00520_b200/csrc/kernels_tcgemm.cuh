@@ -373,13 +373,15 @@ __global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const int x = t % maxtiles;
     const int sub = (t / maxtiles) % maxsub;
-    const GemmDesc d = descs[t / (maxtiles * maxsub)];
+    GemmDesc d = descs[t / (maxtiles * maxsub)];
     if (sub >= d.batch) continue;                      // uniform over the CTA
     const int tiles_m = (d.m + BM - 1) / BM;
     const int tiles_n = (d.n + BN - 1) / BN;
     if (x >= tiles_m * tiles_n) continue;
     const int m0 = (x % tiles_m) * BM;
     const int n0 = (x / tiles_m) * BN;
+    if (d.Bp)   // pre-split B (k_tc_pack_b<BN>): this tile's chunks
+      d.Bp += ((int64_t)sub * tiles_n + n0 / BN) * ((d.k + TC_BK - 1) / TC_BK) * Cfg::BP_FLOATS;
     const float2* __restrict__ A = d.A + (int64_t)sub * d.sA;
     const float2* __restrict__ B = d.B + (int64_t)sub * d.sB;
     float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
