@@ -510,9 +510,37 @@ static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
   return FMMT_OK;
 }
 
+// A per-direction descriptor whose A and B are both static factors (Tucker-3D mode-1: core_p, U1_p;
+// TT-3D head: C1_p, U1_p): pre-split both once per op (asynchronous; build_plans synchronises).
+static fmmt_status with_packed_static(fmmt_op* op, GemmDesc& d) {
+  fmmt_ctx* ctx = op->ctx;
+  if (!ctx->pack_b || !ctx->pack_factors || ctx->gemm_impl != 1 || ctx->warp_specialised) return FMMT_OK;
+  const int64_t tiles_m = (d.m + fmmt::TC_BM - 1) / fmmt::TC_BM, nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
+  const int64_t fa = tiles_m * nkc * fmmt::TC_PACK_FLOATS, fb = packb_floats(d);
+  float* buf = nullptr;
+  if (cudaMalloc(&buf, (fa + fb) * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, FMMT_E_NOMEM, "pre-split operand allocation (%lld B) failed", (long long)((fa + fb) * 4));
+  }
+  op->pack_bytes += (fa + fb) * 4;
+  op->bpk_static.push_back(buf);
+  {
+    ProfScope ps(ctx, "pack_a");
+    const int64_t work = tiles_m * fmmt::TC_BM * nkc * (fmmt::TC_BK / 2);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 16));
+    fmmt::k_tc_pack_a<<<blocks, 256, 0, ctx->stream>>>(d, buf);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  }
+  if (fmmt_status st = launch_pack_b(ctx, d, buf + fa)) return st;
+  d.Ap = buf;
+  d.a_nkc = (int)nkc;
+  d.Bp = buf + fa;
+  return FMMT_OK;
+}
+
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
-static void tucker_chain(fmmt_op* op, Batch& b) {
+static fmmt_status tucker_chain(fmmt_op* op, Batch& b) {
   // Fig. 3(a) in the "tall" orientation so every GEMM has >= n1*r rows:
   //   mode 1:  H_q[(b + r2 c) + r2 r3 i] = sum_a core_q[a + r1 (b + r2 c)] U1[i + n1 a]
   //   mode 2:  G_q[i + n1 j + n12 c]     = sum_b H_q[b + r2 c + r2 r3 i] U2[j + n2 b]
@@ -528,7 +556,9 @@ static void tucker_chain(fmmt_op* op, Batch& b) {
       const float2* U2 = op->arr[2] + op->off[2][p];
       float2* Hq = op->H + q * n1 * op->r2max * op->r3max;
       float2* Gq = op->Gw + q * n12 * op->rGmax;
-      sa.push_back(gdx(core, U1, Hq, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3));
+      GemmDesc d1 = gdx(core, U1, Hq, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3);
+      if (fmmt_status st = with_packed_static(op, d1)) return st;
+      sa.push_back(d1);
       sb.push_back(gdx(Hq, U2, Gq, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1));
     }
   } else {
@@ -542,6 +572,7 @@ static void tucker_chain(fmmt_op* op, Batch& b) {
   }
   add_gemm(op, b, sa, "restore_mode1");
   add_gemm(op, b, sb, "restore_mode2");
+  return FMMT_OK;
 }
 
 static fmmt_status ensure_zscr(fmmt_op* op);
@@ -595,7 +626,9 @@ static fmmt_status build_plans(fmmt_op* op) {
     b.nq = (int)std::min<int64_t>(PB, op->ndir - q0);
     switch (op->format) {
       case FMMT_DENSE: break;
-      case FMMT_TUCKER3D: tucker_chain(op, b); break;
+      case FMMT_TUCKER3D:
+        if ((st = tucker_chain(op, b))) return st;
+        break;
       case FMMT_TUCKER4D: {
         const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3);
         // a3 (Fig. 3(b)): C_q = C(r1 r2 r3 x r4) . U4[p,:]^T
@@ -603,7 +636,7 @@ static fmmt_status build_plans(fmmt_op* op) {
         if ((st = with_packed_a(op, 0, ds))) return st;
         if ((st = with_packed_b_static(op, ds))) return st;
         add_gemm(op, b, {ds}, "slice_tucker4d");
-        tucker_chain(op, b);
+        if ((st = tucker_chain(op, b))) return st;
         break;
       }
       case FMMT_HTUCKER4D: {
@@ -649,8 +682,10 @@ static fmmt_status build_plans(fmmt_op* op) {
         for (int q = 0; q < b.nq; ++q) {
           const int64_t p = b.q0 + q;
           const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1);
-          ds.push_back(gdx(op->arr[1] + op->off[1][p], op->arr[0] + op->off[0][p], op->Gw + q * n12 * op->rGmax,
-                           n2 * r2, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, n12, n2, 1));
+          GemmDesc dh = gdx(op->arr[1] + op->off[1][p], op->arr[0] + op->off[0][p], op->Gw + q * n12 * op->rGmax,
+                            n2 * r2, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, n12, n2, 1);
+          if ((st = with_packed_static(op, dh))) return st;
+          ds.push_back(dh);
         }
         add_gemm(op, b, ds, "restore_tt_head");
         break;
@@ -673,6 +708,7 @@ static fmmt_status build_plans(fmmt_op* op) {
     op->zscr_elems = 0;
   }
   if ((st = ensure_zscr(op))) return st;
+  FMMT_CUDA(op->ctx, cudaStreamSynchronize(op->ctx->stream));   // static pre-splits done
   if (!op->descs.empty()) {
     FMMT_CUDA(op->ctx, cudaMalloc(&op->d_descs, op->descs.size() * sizeof(GemmDesc)));
     FMMT_CUDA(op->ctx, cudaMemcpy(op->d_descs, op->descs.data(), op->descs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
