@@ -376,6 +376,7 @@ static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, con
     L.tc_maxtiles = std::max(L.tc_maxtiles, ((d.m + fmmt::TC_BM - 1) / fmmt::TC_BM) * ((d.n + L.tc_bn - 1) / L.tc_bn));
     L.maxsub = std::max(L.maxsub, d.batch);
     op->descs.push_back(d);
+    op->descs.back().n_fast = d.m > d.n ? 1 : 0;   // stream the larger operand once (A: m x k, B: k x n)
   }
   b.gemms.push_back(L);
 }
@@ -953,6 +954,23 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     a.Tout = Tout;
     if (mode != fmmt::Z_RESTORE && (!op->zscr || op->zscr_elems < (int64_t)nq * ncomp * (op->n3 / 2) * a.n12))
       return set_err(ctx, FMMT_E_STATE, "z scratch not allocated");
+    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b) {
+      // pre-split V_q per parity pass h (columns kz = 2j + h) into Vpk[h][q]
+      using PC = fmmt::TcGemmCfg<32, 1>;
+      const int k = a.rank;
+      const int64_t per_q = ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * PC::BP_FLOATS;
+      if (op->vpk_floats < 2 * per_q * nq)
+        return set_err(ctx, FMMT_E_STATE, "pre-split V workspace too small");
+      ProfScope ps2(ctx, "pack_v");
+      const int64_t items = (int64_t)nq * ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * 32 * (fmmt::TC_BK / 2);
+      const unsigned g2 = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
+      for (int h = 0; h < 2; ++h)
+        fmmt::k_tc_pack_b<32><<<g2, 256, 0, ctx->stream>>>(a.V + (int64_t)h * a.v_sk, a.v_stride, a.v_sc, 2 * a.v_sk, k,
+                                                            32, nq, op->Vpk + (int64_t)h * nq * per_q);
+      FMMT_CUDA(ctx, cudaGetLastError());
+      a.Vp = op->Vpk;
+      a.vp_stride = per_q;
+    }
     static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
                                    "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
@@ -1049,11 +1067,12 @@ static fmmt_status ensure_zscr(fmmt_op* op) {
 // TT-4D z-stage pre-split V_q workspace (pack_v) for the largest batch.
 static fmmt_status ensure_vpk(fmmt_op* op) {
   fmmt_ctx* ctx = op->ctx;
-  if (op->format != FMMT_TT4D || !ctx->pack_b || op->n3 > 32) return FMMT_OK;
+  if (op->format != FMMT_TT4D || !ctx->pack_b || op->n3 > 64) return FMMT_OK;
   int64_t nq = 1;
   for (const Batch& b : op->batches) nq = std::max<int64_t>(nq, b.nq);
   const int BN = op->n3 <= 16 ? 16 : 32;
-  const int64_t nkc = (rk(op, 0, 1) + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (op->n3 + BN - 1) / BN;
+  const int64_t nkc = (rk(op, 0, 1) + fmmt::TC_BK - 1) / fmmt::TC_BK;
+  const int64_t tiles_n = op->n3 == 64 ? 2 : (op->n3 + BN - 1) / BN;   // n3 = 64: one 32-column pack per parity pass
   const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK);   // BP_FLOATS = 2 NR x 2 BK, NR = 2 BN
   if (op->vpk_floats >= need) return FMMT_OK;
   cudaStreamSynchronize(ctx->stream);

@@ -36,6 +36,9 @@ struct GemmDesc {
   // optional pre-split B (k_tc_pack_b) of this tile's columns: chunk c at Bp + c * TcGemmCfg::BP_FLOATS
   // (set per tile by the kernel); nullptr = none
   const float* Bp;
+  // tensor-core tile order: 0 = m-tiles fastest (B tile shared by consecutive CTAs), 1 = n-tiles fastest
+  // (A tile shared; chosen when A is the larger operand, so it streams from DRAM once)
+  int n_fast;
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {

@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict
     const int tiles_m = (d.m + BM - 1) / BM;
     const int tiles_n = (d.n + BN - 1) / BN;
     if (x >= tiles_m * tiles_n) continue;
-    const int m0 = (x % tiles_m) * BM;
-    const int n0 = (x / tiles_m) * BN;
+    const int m0 = (d.n_fast ? x / tiles_n : x % tiles_m) * BM;
+    const int n0 = (d.n_fast ? x % tiles_n : x / tiles_m) * BN;
     if (d.Bp)   // pre-split B (k_tc_pack_b<BN>): this tile's chunks
       d.Bp += ((int64_t)sub * tiles_n + n0 / BN) * ((d.k + TC_BK - 1) / TC_BK) * Cfg::BP_FLOATS;
     const float2* __restrict__ A = d.A + (int64_t)sub * d.sA;
@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
   float acc[2 * BN];
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
+    d.Bp = a.Vp ? a.Vp + ((int64_t)h * nq + q) * a.vp_stride : nullptr;   // pre-split V_q columns 2j + h
     tc_mainloop<BN, 1>(d, A, B, m0, h * H, tcsm, bar, tmem, acc, cur);   // T_p[ij, 2m + h]
     if constexpr (MODE == Z_RESTORE) {
       if (valid) {
