@@ -854,6 +854,8 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
       break;
     case FMMT_TT4D:
       a.G = op->tbar1; a.g_stride = 0; a.Gp = op->tbar1_pk;
+      // T1 pre-split = 16 B per complex: block the z-stage tiles by direction when it exceeds ~1/4 of L2
+      a.z_blocked = n12 * rk(op, 0, 1) * 16 > (32ll << 20) ? 1 : 0;
       a.V = op->Vw; a.v_stride = rk(op, 0, 1) * op->n3; a.v_sc = 1; a.v_sk = rk(op, 0, 1); a.rank = (int)rk(op, 0, 1);
       break;
   }

@@ -318,6 +318,7 @@ struct ZArgs {
   int rank;                  // uniform rank when rank_p == nullptr
   const float* Vp;           // V pre-split for the tensor-core kernel (k_tc_pack_b), or nullptr
   int64_t vp_stride;         // floats per batch-local q
+  int z_blocked;             // tensor-core z-stage: direction-blocked tile order (shared A larger than L2 share)
   // dense operator: T[p][k][ij]
   const float2* T;
   // restore output [k][ij]

@@ -33,6 +33,25 @@
 
 namespace fmmt {
 
+// z-stage tile order.  Tile t of tiles_m x nq (m-tile, direction q).  With a per-direction A (3D formats)
+// q-major order keeps each direction's operands together.  With a shared A (TT-4D T1) too large to stay
+// in L2 (ZArgs::z_blocked, set by the host) the directions are taken in blocks of ZQB: within a block the
+// m-tile is the slow index, so consecutive CTAs share one A tile through L2 and the block's pre-split V_q
+// stay L2-resident while the m-tiles sweep (T1 streams from HBM once per block, not once per direction).
+constexpr int ZQB = 16;
+__device__ __forceinline__ void z_tile(int t, int tiles_m, int nq, bool shared_a, int& q, int& mt) {
+  if (!shared_a) {
+    q = t / tiles_m;
+    mt = t % tiles_m;
+    return;
+  }
+  const int qb = t / (tiles_m * ZQB);
+  const int r = t - qb * tiles_m * ZQB;
+  const int qbs = min(ZQB, nq - qb * ZQB);
+  mt = r / qbs;
+  q = qb * ZQB + r % qbs;
+}
+
 constexpr int TC_BM = 128;      // rows per tile (UMMA M)
 constexpr int TC_BK = 8;        // complex K per chunk (16 real = 2 UMMA K-steps)
 constexpr int TC_NS = 4;        // operand ring stages: copies run 2 chunks ahead, MMAs of chunk k-1 overlap
@@ -431,10 +450,12 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
   TcCursor cur;
   // tiles t = (m-tile, direction group), walked by this CTA with one TMEM allocation
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
-    const int q0 = (t / tiles_m) * ND;
+    int qg, mt;
+    z_tile(t, tiles_m, (nq + ND - 1) / ND, ND == 1 && a.z_blocked, qg, mt);
+    const int q0 = qg * ND;
     const int p0 = a.p0 + q0;
     const int nd = min(ND, nq - q0);
-    const int m0 = (t % tiles_m) * TC_BM;
+    const int m0 = mt * TC_BM;
     GemmDesc d;
     d.m = (int)a.n12;
     d.n = nd * N3;
@@ -507,9 +528,10 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
   const uint32_t tmem = tc_setup<Cfg::TMEM_COLS>(bar, &tslot);
   TcCursor cur;
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
-  const int q = t / tiles_m;
+  int q, mt;
+  z_tile(t, tiles_m, nq, a.z_blocked, q, mt);
   const int p = a.p0 + q;
-  const int m0 = (t % tiles_m) * TC_BM;
+  const int m0 = mt * TC_BM;
   GemmDesc d;
   d.m = (int)a.n12;
   d.n = N3;
