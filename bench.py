@@ -423,6 +423,8 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 3), "unit": "Gdir*pt/s",
                 "h2d_bytes_per_step": int(len(ops) * (ndir * K * 8 + ndir * 4)),
                 "d2h_bytes_per_step": int(len(ops) * K * 8)},
+        "per_box": {"value": round(value / 8, 3), "unit": "Gdir*box/s",
+                    "note": "the same rate per box of the Nx*Ny*Nz grid (the padded grid point unit is 8 per box)"},
         "dense_ms": round(dense_ms, 4),
         "two_component": {"value": round(2 * total_units / (two_comp_ms * 1e-3) / 1e9, 3), "unit": "Gdir*pt/s",
                           "ms_per_step": round(two_comp_ms, 4),
