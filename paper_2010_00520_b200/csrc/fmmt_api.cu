@@ -1280,6 +1280,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
   if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
   if (const char* e = getenv("FMMT_PACKB")) ctx->pack_b = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_AGG_STAGED")) ctx->agg_staged = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_WS")) ctx->warp_specialised = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -1602,10 +1603,21 @@ static fmmt_status aggregate_impl(fmmt_ctx* ctx, const float2* P, const float2* 
   // a warp per (box, block of AGG_PD directions); the generic kernel: a warp per (box, direction)
   const dim3 grid((unsigned)((K + 7) / 8), (unsigned)((ndir + fmmt::AGG_PD - 1) / fmmt::AGG_PD));
   const dim3 grid_any((unsigned)((K + 7) / 8), (unsigned)std::min<int64_t>(ndir, 65535));
+  const dim3 grid_s((unsigned)K, (unsigned)((ndir + 31) / 32));   // shared-memory staged: a CTA per (box, 32 dirs)
+  const bool staged = ctx->agg_staged;
   switch (ncomp) {
-    case 1: fmmt::k_aggregate<1><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
-    case 2: fmmt::k_aggregate<2><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
-    case 4: fmmt::k_aggregate<4><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig); break;
+    case 1:
+      if (staged) fmmt::k_aggregate_smem<1><<<grid_s, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      else fmmt::k_aggregate<1><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      break;
+    case 2:
+      if (staged) fmmt::k_aggregate_smem<2><<<grid_s, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      else fmmt::k_aggregate<2><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      break;
+    case 4:
+      if (staged) fmmt::k_aggregate_smem<4><<<grid_s, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      else fmmt::k_aggregate<4><<<grid, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, K, sig);
+      break;
     default: fmmt::k_aggregate_any<<<grid_any, 256, 0, ctx->stream>>>(P, I, box_ptr, ndir, N, ncomp, K, sig);
   }
   FMMT_CUDA(ctx, cudaGetLastError());

@@ -32,6 +32,7 @@ struct fmmt_ctx {
   bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)
   int tc_ctas_per_sm = 4;           // tensor-core GEMM grid: CTAs per SM (each loops over tiles)
   bool warp_specialised = false;    // tensor-core kernels: producer / consumer warps, 1 CTA/SM (FMMT_WS)
+  bool agg_staged = true;           // aggregation: shared-memory staged kernel (FMMT_AGG_STAGED=0: warp-per-box)
   void* agg_part = nullptr;         // disaggregation partial sums [nsplit][N] (complex64)
   int64_t agg_part_elems = 0;
   std::vector<fmmt_prof_entry> pending;

@@ -167,6 +167,57 @@ __global__ void __launch_bounds__(256) k_aggregate(const float2* __restrict__ P,
   }
 }
 
+// Aggregation staged through shared memory: one CTA (256 threads) per box v and block of 32
+// directions.  Per pass of up to AGS_F / NC basis functions the CTA copies the 32 directions' contiguous
+// pattern rows P[p][n0:n1][:] into shared memory with coalesced 16-byte loads, then thread (np, c, d)
+// (d = direction, lane-fastest; c = component; np = quarter of the pass) sums its quarter of
+// P[d][n][c] I[n] from shared memory; the quarters are added through shared memory and lane d of the
+// first NC warps writes sig[p][c][v].  No shuffles, few index operations per element.
+constexpr int AGS_F = 128;   // staged float2 per direction row and pass (AGS_F / NC basis functions; boxes hold ~55)
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_aggregate_smem(const float2* __restrict__ P, const float2* __restrict__ I,
+                                                        const int64_t* __restrict__ box_ptr, int64_t ndir, int64_t N,
+                                                        int64_t K, float2* __restrict__ sig) {
+  static_assert(NC == 1 || NC == 2 || NC == 4, "components per basis function");
+  constexpr int NP = 8 / NC;                     // n-parts: 32 directions x NC components x NP = 256 threads
+  constexpr int AGS_N = AGS_F / NC;              // basis functions per pass
+  constexpr int ROW = AGS_F + 1;                 // float2 per staged direction row (odd: no bank conflicts)
+  __shared__ float2 sP[32 * ROW];
+  __shared__ float2 sI[AGS_N];
+  __shared__ float2 red[256];
+  const int64_t v = blockIdx.x;
+  const int64_t p0 = (int64_t)blockIdx.y * 32;
+  const int tid = threadIdx.x;
+  const int d = tid & 31, c = (tid >> 5) % NC, np = (tid >> 5) / NC;
+  const int64_t lo = box_ptr[v], hi = box_ptr[v + 1];
+  float2 acc = make_float2(0.f, 0.f);
+  for (int64_t n0 = lo; n0 < hi; n0 += AGS_N) {
+    const int m = (int)(hi - n0 < AGS_N ? hi - n0 : AGS_N);
+    __syncthreads();                              // previous pass's reads done
+    // stage: 32 rows of m * NC float2 (row r = direction p0 + r), coalesced along the row
+    for (int e = tid; e < 32 * m * NC; e += 256) {
+      const int r = e / (m * NC), o = e - r * (m * NC);
+      const int64_t p = p0 + r;
+      sP[r * ROW + o] = p < ndir ? __ldg(P + (p * N + n0) * NC + o) : make_float2(0.f, 0.f);
+    }
+    for (int e = tid; e < m; e += 256) sI[e] = __ldg(I + n0 + e);
+    __syncthreads();
+    // thread (np, c, d): n = np, np + NP, ... of this pass
+    const float2* row = sP + d * ROW + c;
+    for (int n = np; n < m; n += NP) cmac(acc, row[n * NC], sI[n]);
+  }
+  red[tid] = acc;
+  __syncthreads();
+  if (tid < 32 * NC) {                            // np == 0 threads: add the other quarters, write
+    float2 t = red[tid];
+#pragma unroll
+    for (int q = 1; q < NP; ++q) t = cadd(t, red[tid + q * 32 * NC]);
+    const int64_t p = p0 + d;
+    if (p < ndir) sig[(p * NC + c) * K + v] = t;
+  }
+}
+
 // Generic-ncomp aggregation (one component pass at a time): the fallback for ncomp not in {1, 2, 4}.
 __global__ void __launch_bounds__(256) k_aggregate_any(const float2* __restrict__ P, const float2* __restrict__ I,
                                                        const int64_t* __restrict__ box_ptr, int64_t ndir, int64_t N,
