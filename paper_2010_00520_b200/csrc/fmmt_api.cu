@@ -1626,7 +1626,8 @@ static fmmt_status aggregate_impl(fmmt_ctx* ctx, const float2* P, const float2* 
 
 // direction blocks of the disaggregation: up to 16 (non-empty boxes x blocks fill the SMs; the partial
 // sums add 16 N complex writes + reads against the ndir N ncomp complex pattern reads)
-static int agg_nsplit(const fmmt_ctx*, int64_t ndir, int64_t) {
+static int agg_nsplit(const fmmt_ctx* ctx, int64_t ndir, int64_t) {
+  if (ctx->agg_staged) return (int)((ndir + 31) / 32);                  // k_disaggregate_smem: 32 per block
   return (int)std::max<int64_t>(1, std::min<int64_t>(16, ndir / 16));   // >= 16 directions per block
 }
 
@@ -1639,7 +1640,11 @@ static fmmt_status disaggregate_impl(fmmt_ctx* ctx, const float2* P, const float
   {
     ProfScope ps(ctx, "disaggregate_partial");
     const dim3 grid((unsigned)K, (unsigned)nsplit);
-    switch (ncomp) {
+    if (ctx->agg_staged && (ncomp == 1 || ncomp == 2 || ncomp == 4)) {   // nsplit = ceil(ndir / 32)
+      if (ncomp == 1) fmmt::k_disaggregate_smem<1><<<grid, 256, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, part);
+      else if (ncomp == 2) fmmt::k_disaggregate_smem<2><<<grid, 256, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, part);
+      else fmmt::k_disaggregate_smem<4><<<grid, 256, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, part);
+    } else switch (ncomp) {
       case 1: fmmt::k_disaggregate_partial<1><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;
       case 2: fmmt::k_disaggregate_partial<2><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;
       case 4: fmmt::k_disaggregate_partial<4><<<grid, 64, 0, ctx->stream>>>(P, B, w, box_ptr, ndir, N, K, nsplit, part); break;

@@ -288,6 +288,75 @@ __global__ void __launch_bounds__(64) k_disaggregate_partial(const float2* __res
   }
 }
 
+// Partial disaggregation staged through shared memory: one CTA (256 threads) per box v and block s of
+// 32 directions (nsplit = ceil(ndir / 32)).  Per pass of up to AGS_F / NC basis functions the CTA copies
+// the 32 directions' pattern rows (coalesced) and w_p B[p][:][v] into shared memory; thread (dq, m)
+// (m = basis function of the pass, fastest; dq = quarter of the 32 directions) sums
+// w_p conj(P[p][m][c]) B[p][c][v] over its 8 directions; the quarters are added through shared memory:
+//   part[s][m] = sum_{p in block s} w_p sum_c conj(P[p][m][c]) B[p][c][v].
+template <int NC>
+__global__ void __launch_bounds__(256) k_disaggregate_smem(const float2* __restrict__ P, const float2* __restrict__ B,
+                                                           const float* __restrict__ w,
+                                                           const int64_t* __restrict__ box_ptr, int64_t ndir,
+                                                           int64_t N, int64_t K, float2* __restrict__ part) {
+  static_assert(NC == 1 || NC == 2 || NC == 4, "components per basis function");
+  constexpr int AGS_N = AGS_F / NC;              // basis functions per pass (64 for NC = 2)
+  constexpr int ROW = AGS_F + 1;
+  constexpr int MT = AGS_N < 64 ? AGS_N : 64;    // threads along m
+  constexpr int DQ = 256 / MT;                   // direction parts
+  __shared__ float2 sP[32 * ROW];
+  __shared__ float2 sB[32 * NC];
+  __shared__ float2 red[256];
+  const int64_t v = blockIdx.x;
+  const int s = blockIdx.y;
+  const int64_t p0 = (int64_t)s * 32;
+  const int tid = threadIdx.x;
+  const int ml = tid % MT, dq = tid / MT;
+  const int64_t lo = box_ptr[v], hi = box_ptr[v + 1];
+  if (hi == lo) return;
+  if (tid < 32 * NC) {                            // w_p B[p][c][v] of the block's directions
+    const int r = tid / NC, c = tid % NC;
+    const int64_t p = p0 + r;
+    float2 b = make_float2(0.f, 0.f);
+    if (p < ndir) {
+      b = __ldg(B + (p * NC + c) * K + v);
+      const float wp = __ldg(w + p);
+      b.x *= wp;
+      b.y *= wp;
+    }
+    sB[tid] = b;
+  }
+  for (int64_t n0 = lo; n0 < hi; n0 += AGS_N) {
+    const int m = (int)(hi - n0 < AGS_N ? hi - n0 : AGS_N);
+    __syncthreads();                              // previous pass's reads done (and sB written)
+    for (int e = tid; e < 32 * m * NC; e += 256) {
+      const int r = e / (m * NC), o = e - r * (m * NC);
+      const int64_t p = p0 + r;
+      sP[r * ROW + o] = p < ndir ? __ldg(P + (p * N + n0) * NC + o) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int mm0 = 0; mm0 < m; mm0 += MT) {      // uniform trip count (barriers inside)
+      const int mm = mm0 + ml;
+      float2 acc = make_float2(0.f, 0.f);
+      if (mm < m) {
+#pragma unroll 4
+        for (int r = dq; r < 32; r += DQ)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) cmac_conj(acc, sP[r * ROW + mm * NC + c], sB[r * NC + c]);
+      }
+      red[tid] = acc;
+      __syncthreads();
+      if (dq == 0 && mm < m) {
+        float2 t = red[ml];
+#pragma unroll
+        for (int q = 1; q < DQ; ++q) t = cadd(t, red[ml + q * MT]);
+        part[(int64_t)s * N + n0 + mm] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Generic-ncomp partial disaggregation (fallback for ncomp not in {1, 2, 4}).
 __global__ void __launch_bounds__(64) k_disaggregate_partial_any(const float2* __restrict__ P,
                                                                  const float2* __restrict__ B,
