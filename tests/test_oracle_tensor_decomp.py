@@ -178,3 +178,23 @@ def test_table2_ranks(golden_dir):
     f = decomp.tucker_svd(T4, g["gamma"])
     assert f.ranks[3] == g["tucker4d_r4"]
     assert all(abs(r - g["tucker4d_r123"]) <= tol(g["tucker4d_r123"]) for r in f.ranks[:3])
+
+
+@pytest.mark.slow
+def test_table2_tucker3d_exact_at_effective_gamma(golden_dir):
+    """Table II's Tucker-3D r_max = 29 (n = 32, 435 directions) is reproduced exactly by the oracle's
+    Alg. 1 (reading Q7) at gamma = 1e-5, and exceeded (31) at the stated 1e-6: the printed ranks are
+    consistent with an effective tolerance one decade looser than stated."""
+    g = json.load(open(os.path.join(golden_dir, "table2.json")))
+    N = g["n"] // 2
+    grid = fmm.OperatorGrid(N, N, N, g["edge"], 2 * np.pi, g["L"])
+    khat, _, _, _ = fmm.direction_grid(g["L"], g["nphi"])
+    rmax_eff, rmax_stated = 0, 0
+    for p in range(len(khat)):
+        t = fmm.fft_operator_3d(grid, khat[p])
+        rmax_eff = max(rmax_eff, max(decomp.tucker_svd(t, g["effective_gamma"]).ranks))
+        if p % 29 == 0:
+            rmax_stated = max(rmax_stated, max(decomp.tucker_svd(t, g["gamma"]).ranks))
+    assert rmax_eff == g["tucker3d_rmax"]
+    assert rmax_stated > g["tucker3d_rmax"]
+
