@@ -319,3 +319,36 @@ def test_single_direction_and_batching_invariance(fm, ctx):
     op1.close()
     sm = translate.sig_to_math(sig)
     assert rel(cp.translate(sm, 5), translate.sig_to_math(out1)[0]) <= TRANSLATE_TOL
+
+
+@pytest.mark.parametrize("fmt", ["tucker3d", "tt3d", "tucker4d", "htucker4d", "tt4d"])
+def test_degenerate_operators(fm, ctx, fmt):
+    """Degenerate inputs (SURVEY §8(b) conventions): an all-zero operator compresses to rank-1 zero factors
+    and translates to exactly zero; a rank-1 operator (outer product of random vectors, direction mode
+    included) compresses to rank 1 everywhere and translates within the bar of the oracle."""
+    n = (8, 8, 8)
+    nd = 5
+    N = (4, 4, 4)
+    sig = signatures(5, nd, *N)
+    d_in = dev(sig)
+    d_out = torch.empty_like(d_in)
+    # zero
+    op = ctx.compress(np.zeros((nd,) + n[::-1], np.complex128), n, nd, fmt, 1e-4)
+    assert np.all(op.ranks() == 1)
+    d_out.fill_(1.0)
+    op.translate(d_in, d_out, nd, N)
+    ctx.sync()
+    assert not torch.any(d_out != 0)
+    op.close()
+    # rank one: T[i,j,k,p] = a_i b_j c_k e_p
+    rng = np.random.default_rng(11)
+    a, b, c3, e = (rng.standard_normal(m) + 1j * rng.standard_normal(m) for m in (*n, nd))
+    T4 = np.einsum("i,j,k,p->ijkp", a, b, c3, e)
+    op = ctx.compress(np.ascontiguousarray(np.transpose(T4, (3, 2, 1, 0))), n, nd, fmt, 1e-6)
+    assert np.all(op.ranks() == 1), op.ranks()
+    op.translate(d_in, d_out, nd, N)
+    ctx.sync()
+    sm, om = translate.sig_to_math(sig), translate.sig_to_math(d_out.cpu().numpy())
+    for p in range(nd):
+        assert rel(translate.translate_fft(T4[..., p], sm[p]), om[p]) <= TRANSLATE_TOL, p
+    op.close()
