@@ -898,7 +898,7 @@ static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& 
   constexpr int G = 1;   // 2 = even/odd kz split over two thread groups (measured slower: 1 CTA/SM by registers)
   using Cfg = fmmt::TcGemmCfg<BN, G>;
   const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)((nq + ND - 1) / ND);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
   if (mode == fmmt::Z_RESTORE) {
     if constexpr (ND == 1) {
       FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G>, Cfg::SMEM));
@@ -991,7 +991,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
     using Cfg = fmmt::TcGemmCfg<32, 1>;
     const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
     if (mode == fmmt::Z_RESTORE) {
       FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z64<fmmt::Z_RESTORE>, Cfg::SMEM));
       fmmt::k_tc_conv_z64<fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, op->zscr, nq);
@@ -1282,6 +1282,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_PACKB")) ctx->pack_b = atoi(e) != 0;
   if (const char* e = getenv("FMMT_AGG_STAGED")) ctx->agg_staged = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_WS")) ctx->warp_specialised = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {

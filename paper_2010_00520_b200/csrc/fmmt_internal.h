@@ -31,6 +31,7 @@ struct fmmt_ctx {
   bool pack_b = true;               // TT-4D z-stage: pre-split V_q per batch (FMMT_PACKB=0 disables)
   bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)
   int tc_ctas_per_sm = 2;           // tensor-core GEMM grid: CTAs per SM = the resident count (each loops over tiles)
+  int tc_ctas_z = 4;                // tensor-core z-stage grid: CTAs per SM (two waves measured faster there)
   bool warp_specialised = false;    // tensor-core kernels: producer / consumer warps, 1 CTA/SM (FMMT_WS)
   bool agg_staged = true;           // aggregation: shared-memory staged kernel (FMMT_AGG_STAGED=0: warp-per-box)
   void* agg_part = nullptr;         // disaggregation partial sums [nsplit][N] (complex64)
