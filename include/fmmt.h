@@ -205,7 +205,10 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info);
  * *count = number of int64 written (fails with FMMT_E_ARG if cap is short). */
 fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_t* count);
 
-/* Number of directions per internal batch (workspace is resized). 0 = auto. */
+/* Number of directions per internal batch (workspace and the per-plan pre-split
+ * operand buffers are rebuilt).  0 = auto: batches whose rank-sized intermediates
+ * fit ~48 MB (L2), enlarged for the 4D formats until the shared slice operand
+ * streamed once per batch no longer dominates (<= 4 GB of intermediates). */
 fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs_per_batch);
 
 /* ------------------------------------------------------------ the hot path */

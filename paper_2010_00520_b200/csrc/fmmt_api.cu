@@ -248,6 +248,7 @@ struct fmmt_op {
   float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
   std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
   int64_t pack_bytes = 0;
+  int64_t packb_bytes = 0;                      // per-plan pre-split B buffers (bpk_static, Mpk)
   int64_t w_ncomp = 1;                         // signature components W is allocated for
   float2* zscr = nullptr;                      // n3 = 64 tensor-core z-stage: even-pass partials (batch)
   int64_t zscr_elems = 0;
@@ -503,7 +504,7 @@ static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
     cudaGetLastError();
     return set_err(ctx, FMMT_E_NOMEM, "pre-split B allocation (%lld B) failed", (long long)(floats * 4));
   }
-  op->pack_bytes += floats * 4;
+  op->packb_bytes += floats * 4;
   op->bpk_static.push_back(buf);
   if (fmmt_status st = launch_pack_b(ctx, d, buf)) return st;
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -523,7 +524,7 @@ static fmmt_status with_packed_static(fmmt_op* op, GemmDesc& d) {
     cudaGetLastError();
     return set_err(ctx, FMMT_E_NOMEM, "pre-split operand allocation (%lld B) failed", (long long)((fa + fb) * 4));
   }
-  op->pack_bytes += (fa + fb) * 4;
+  op->packb_bytes += (fa + fb) * 4;
   op->bpk_static.push_back(buf);
   {
     ProfScope ps(ctx, "pack_a");
@@ -588,6 +589,7 @@ static fmmt_status build_plans(fmmt_op* op) {
   if (op->Mpk) cudaFree(op->Mpk);
   op->Mpk = nullptr;
   op->mpk_floats = 0;
+  op->packb_bytes = 0;
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
   if (op->PB <= 0) {
     // batch size: the per-batch intermediates L2-resident (48 MB) ...
@@ -681,6 +683,7 @@ static fmmt_status build_plans(fmmt_op* op) {
               return set_err(op->ctx, FMMT_E_NOMEM, "pre-split M allocation (%lld B) failed", (long long)(need * 4));
             }
             op->mpk_floats = need;
+            op->packb_bytes += need * 4;
           }
           mpk = op->Mpk;
           dg.Bp = mpk;
@@ -1409,7 +1412,7 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
   info->compressed_bytes = comp * 8;
   info->original_bytes = op->n1 * op->n2 * op->n3 * op->ndir * 8;
   info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0) +
-                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0) + op->pack_bytes;
+                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0) + op->pack_bytes + op->packb_bytes;
   info->batch = op->PB;
   // restore complex MACs per matvec (a3 + a4), in the contraction order the kernels use
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n = n1 * n2 * n3;
