@@ -161,7 +161,16 @@ fmmt_status fmmt_build_operator_lossy(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, int
  * Truncation: r = min{r >= 1 : ||sigma_{r+1:}||_2 <= tol/sqrt(m) ||T||_F},
  *   m = d (Tucker), d-1 (TT), 6 (H-Tucker; reading Q7/Q8).
  * Factors are computed in FP64 (complex128) and rounded to complex64.
- * The op translates dir_count directions.                                   */
+ * The op translates dir_count directions.
+ * Sharded 4D setup (context from fmmt_init_sharded, world > 1): collective over
+ * the communicator.  Rank 0 passes the whole T_4D and compresses it; the other
+ * ranks pass T = NULL.  Rank 0 broadcasts the ranks and factors (ncclBroadcast)
+ * and every rank keeps the direction-factor rows of its own
+ * [dir_begin, dir_begin+dir_count).  If rank 0 fails before the broadcast the
+ * other ranks return FMMT_E_STATE.
+ * Shapes outside the translate path (non-power-of-two n, n3 > 64, one xy plane
+ * above 227 KB of shared memory) give a storage-only op: ranks, info and export
+ * work, translate / restore return FMMT_E_UNSUPPORTED (paper sweeps).       */
 fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t n1, int64_t n2, int64_t n3,
                           int64_t ndir, int64_t dir_begin, int64_t dir_count,
                           fmmt_format format, double tol, fmmt_op** op);
@@ -197,9 +206,19 @@ typedef struct {
   int64_t workspace_bytes;     /* device workspace owned by the op                 */
   int64_t batch;               /* directions per internal batch                    */
   double restore_cmac;         /* complex MACs of restore per matvec (a3 + a4)     */
+  int64_t translatable;        /* 1: translate / restore run; 0: storage-only op   */
 } fmmt_op_info_t;
 
 fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info);
+
+/* Export factor array `index` (0 <= index < the format's array count, the
+ * fmmt_op_import order and layout) as complex64 into dst (host or device memory,
+ * detected; cap elements).  *count = the array's element count; dst == NULL
+ * only queries it.  Synchronises the context stream.  Sharded 4D ops export
+ * their local direction-factor rows.  Parity hook: the GPU compressor's factors
+ * go to the oracle.  Errors: FMMT_E_ARG (index, cap, null count),
+ * FMMT_E_CUDA (copy).                                                            */
+fmmt_status fmmt_op_export(const fmmt_op* op, int64_t index, fmmt_c64* dst, int64_t cap, int64_t* count);
 
 /* Ranks: 3D formats write [ndir][nslots] (per direction), 4D formats nslots.
  * *count = number of int64 written (fails with FMMT_E_ARG if cap is short). */

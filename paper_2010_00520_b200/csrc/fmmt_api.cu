@@ -12,6 +12,7 @@
 // and, for translate_sum, the weighted direction sum (a7) + NCCL allreduce.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,8 +30,6 @@
 #include "kernels_fft.cuh"
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
-#include "kernels_tcgemm_v1.cuh"
-#include "kernels_tcws.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -80,12 +79,14 @@ struct ProfScope {
   cudaEvent_t e0 = nullptr;
   ProfScope(fmmt_ctx* c, const char* n) : ctx(c), name(n) {
     ctx->launches++;
+    nvtxRangePushA(n);   // host-side launch ranges (per-stage NVTX)
     if (ctx->profiling) {
       e0 = take_event(ctx);
       cudaEventRecordWithFlags(e0, ctx->stream, cudaEventRecordExternal);   // graph node when captured
     }
   }
   ~ProfScope() {
+    nvtxRangePop();
     if (ctx->profiling) {
       cudaEvent_t e1 = take_event(ctx);
       cudaEventRecordWithFlags(e1, ctx->stream, cudaEventRecordExternal);
@@ -247,8 +248,6 @@ struct fmmt_op {
   float* tbar1_pk = nullptr;                   // T1 pre-split for the tensor-core z-stage (k_tc_pack_a)
   float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
   std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
-  int64_t pack_bytes = 0;
-  int64_t packb_bytes = 0;                      // per-plan pre-split B buffers (bpk_static, Mpk)
   int64_t w_ncomp = 1;                         // signature components W is allocated for
   float2* zscr = nullptr;                      // n3 = 64 tensor-core z-stage: even-pass partials (batch)
   int64_t zscr_elems = 0;
@@ -257,12 +256,13 @@ struct fmmt_op {
   int64_t sigtmp_elems = 0;
   float2 *W = nullptr, *H = nullptr, *Gw = nullptr, *Cw = nullptr, *Mw = nullptr, *Nw = nullptr,
          *Vw = nullptr, *sigtmp = nullptr, *partial = nullptr;
-  int64_t ws_bytes = 0;
+  // every device buffer the op owns (factors, derived/pre-split operands, workspaces), with its bytes and kind:
+  // fmmt_op_info sums it, fmmt_op_destroy frees what is left
+  std::unordered_map<const void*, std::pair<int64_t, int>> mem;
   int64_t r2max = 1, r3max = 1, rGmax = 1;     // workspace rank bounds
   std::vector<GemmDesc> descs;
   GemmDesc* d_descs = nullptr;
   std::vector<Batch> batches;
-  int nsplit = 1;
   int64_t partial_elems = 0;
   // CUDA graphs of whole matvecs, keyed by the buffers they read / write
   struct GraphEntry {
@@ -272,6 +272,7 @@ struct fmmt_op {
     int64_t launches = 0;   // kernels inside the graph
   };
   std::vector<GraphEntry> graphs;
+  bool translatable = true;                    // false: storage-only op (compress beyond the translate shapes)
   // host staging for translate_sum_host
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
@@ -291,70 +292,87 @@ static int64_t rk(const fmmt_op* op, int64_t p, int slot) {
   return op->ranks[slot];
 }
 
+// Destroy the op's captured matvec graphs (they hold workspace pointers); waits for the stream.
+static void drop_graphs(fmmt_op* op) {
+  cudaStreamSynchronize(op->ctx->stream);
+  for (auto& g : op->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  op->graphs.clear();
+}
+
+enum MemKind { MEM_FACTOR = 0, MEM_DERIVED = 1, MEM_WORKSPACE = 2 };
+
+template <class T>
+static fmmt_status dev_alloc(fmmt_op* op, T** p, int64_t bytes, int kind, const char* what) {
+  *p = nullptr;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, (size_t)std::max<int64_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(op->ctx, FMMT_E_NOMEM, "%s: cudaMalloc(%lld B) failed: %s", what, (long long)bytes, cudaGetErrorString(e));
+  }
+  op->mem[q] = {std::max<int64_t>(bytes, 16), kind};
+  *p = static_cast<T*>(q);
+  return FMMT_OK;
+}
+
+template <class T>
+static void dev_free(fmmt_op* op, T*& p) {
+  if (!p) return;
+  cudaFree((void*)p);
+  op->mem.erase((const void*)p);
+  p = nullptr;
+}
+
+static int64_t mem_bytes(const fmmt_op* op, int kind) {
+  int64_t b = 0;
+  for (auto& kv : op->mem)
+    if (kv.second.second == kind) b += kv.second.first;
+  return b;
+}
+
 static void free_workspace(fmmt_op* op) {
   float2** bufs[] = {&op->W, &op->H, &op->Gw, &op->Cw, &op->Mw, &op->Nw, &op->Vw, &op->sigtmp, &op->partial};
-  for (auto b : bufs) {
-    if (*b) cudaFree(*b);
-    *b = nullptr;
-  }
-  if (op->d_descs) cudaFree(op->d_descs);
-  op->d_descs = nullptr;
-  op->ws_bytes = 0;
+  for (auto b : bufs) dev_free(op, *b);
+  op->partial_elems = 0;
+  op->sigtmp_elems = 0;
+  dev_free(op, op->d_descs);
 }
 
 void fmmt_op_destroy(fmmt_op* op) {
   if (!op) return;
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->stream);
-  free_workspace(op);
-  for (auto a : op->arr)
-    if (a) cudaFree(a);
-  if (op->d_voff) cudaFree(op->d_voff);
-  if (op->d_rank) cudaFree(op->d_rank);
-  if (op->tbar1) cudaFree(op->tbar1);
-  if (op->E) cudaFree(op->E);
-  if (op->zscr) cudaFree(op->zscr);
-  if (op->tbar1_pk) cudaFree(op->tbar1_pk);
-  if (op->E_pk) cudaFree(op->E_pk);
-  for (auto pk : op->arr_pk)
-    if (pk) cudaFree(pk);
   for (auto& g : op->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
-  if (op->d_in_host) cudaFree(op->d_in_host);
-  if (op->d_w_host) cudaFree(op->d_w_host);
-  if (op->d_sum_host) cudaFree(op->d_sum_host);
-  if (op->fA) cudaFree(op->fA);
-  if (op->fB) cudaFree(op->fB);
-  if (op->fPart) cudaFree(op->fPart);
-  if (op->Vpk) cudaFree(op->Vpk);
-  if (op->Mpk) cudaFree(op->Mpk);
-  for (auto b : op->bpk_static)
-    if (b) cudaFree(b);
+  for (auto& kv : op->mem) cudaFree((void*)kv.first);
   delete op;
 }
 
-// per-direction workspace bytes for batch sizing
+// per-direction workspace bytes for batch sizing: every buffer sized by the batch (PB directions)
 static int64_t per_dir_ws(const fmmt_op* op) {
-  const int64_t n12 = op->n1 * op->n2, Nz = op->n3 / 2;
-  int64_t e = 0;   // (W, the half-padded spectra, is allocated for all directions)
-  (void)Nz;
+  const int64_t n12 = op->n1 * op->n2;
+  int64_t e = 0;   // complex elements (W, the half-padded spectra, is allocated for all directions)
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D: e += op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
     case FMMT_TUCKER4D: e += rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) + op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
     case FMMT_HTUCKER4D: e += rk(op, 0, 2) * rk(op, 0, 5) + n12 * op->r3max; break;
     case FMMT_TT3D: e += n12 * op->rGmax; break;
-    case FMMT_TT4D: e += rk(op, 0, 1) * op->n3; break;
+    case FMMT_TT4D: {
+      e += rk(op, 0, 1) * op->n3;
+      // pre-split V_q (pack_v): 4 floats per complex per B' row pair, padded to 8-complex K chunks
+      const int64_t nkc = (rk(op, 0, 1) + 7) / 8;
+      e += nkc * 8 * op->n3 * 2;
+      break;
+    }
   }
+  if (op->n3 == 64 && op->format != FMMT_DENSE) e += op->w_ncomp * 32 * n12;   // zscr (n3 = 64 z-stage)
   return e * 8;
 }
 
 static fmmt_status cmalloc(fmmt_op* op, float2** p, int64_t elems) {
-  if (elems <= 0) elems = 1;
-  cudaError_t e = cudaMalloc(p, elems * sizeof(float2));
-  if (e != cudaSuccess) return set_err(op->ctx, FMMT_E_NOMEM, "cudaMalloc(%lld B) failed: %s", (long long)(elems * 8), cudaGetErrorString(e));
-  op->ws_bytes += elems * 8;
-  return FMMT_OK;
+  return dev_alloc(op, p, std::max<int64_t>(elems, 1) * 8, MEM_WORKSPACE, "workspace");
 }
 
 static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, const char* name) {
@@ -441,12 +459,7 @@ static fmmt_status pack_a(fmmt_op* op, const GemmDesc& d, float** out) {
   fmmt_ctx* ctx = op->ctx;
   const int64_t tiles_m = (d.m + fmmt::TC_BM - 1) / fmmt::TC_BM, nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
   const int64_t floats = tiles_m * nkc * fmmt::TC_PACK_FLOATS;
-  if (cudaMalloc(out, floats * sizeof(float)) != cudaSuccess) {
-    cudaGetLastError();
-    *out = nullptr;
-    return set_err(ctx, FMMT_E_NOMEM, "packed operand allocation (%lld B) failed", (long long)(floats * 4));
-  }
-  op->pack_bytes += floats * 4;
+  if (fmmt_status st = dev_alloc(op, out, floats * 4, MEM_DERIVED, "packed operand")) return st;
   const int64_t work = tiles_m * fmmt::TC_BM * nkc * (fmmt::TC_BK / 2);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 16));
   {
@@ -497,14 +510,10 @@ static fmmt_status launch_pack_b(fmmt_ctx* ctx, const GemmDesc& d, float* out) {
 // A descriptor whose B operand is static (factor rows of this batch): pre-split it once per op (synchronous).
 static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
   fmmt_ctx* ctx = op->ctx;
-  if (!ctx->pack_b || ctx->gemm_impl != 1 || ctx->warp_specialised || !d.Ap) return FMMT_OK;
+  if (!ctx->pack_b || ctx->gemm_impl != 1 || !d.Ap) return FMMT_OK;
   float* buf = nullptr;
   const int64_t floats = packb_floats(d);
-  if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) {
-    cudaGetLastError();
-    return set_err(ctx, FMMT_E_NOMEM, "pre-split B allocation (%lld B) failed", (long long)(floats * 4));
-  }
-  op->packb_bytes += floats * 4;
+  if (fmmt_status st = dev_alloc(op, &buf, floats * 4, MEM_DERIVED, "pre-split B")) return st;
   op->bpk_static.push_back(buf);
   if (fmmt_status st = launch_pack_b(ctx, d, buf)) return st;
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -516,15 +525,11 @@ static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
 // TT-3D head: C1_p, U1_p): pre-split both once per op (asynchronous; build_plans synchronises).
 static fmmt_status with_packed_static(fmmt_op* op, GemmDesc& d) {
   fmmt_ctx* ctx = op->ctx;
-  if (!ctx->pack_b || !ctx->pack_factors || ctx->gemm_impl != 1 || ctx->warp_specialised) return FMMT_OK;
+  if (!ctx->pack_b || !ctx->pack_factors || ctx->gemm_impl != 1) return FMMT_OK;
   const int64_t tiles_m = (d.m + fmmt::TC_BM - 1) / fmmt::TC_BM, nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
   const int64_t fa = tiles_m * nkc * fmmt::TC_PACK_FLOATS, fb = packb_floats(d);
   float* buf = nullptr;
-  if (cudaMalloc(&buf, (fa + fb) * sizeof(float)) != cudaSuccess) {
-    cudaGetLastError();
-    return set_err(ctx, FMMT_E_NOMEM, "pre-split operand allocation (%lld B) failed", (long long)((fa + fb) * 4));
-  }
-  op->packb_bytes += (fa + fb) * 4;
+  if (fmmt_status st = dev_alloc(op, &buf, (fa + fb) * 4, MEM_DERIVED, "pre-split operands")) return st;
   op->bpk_static.push_back(buf);
   {
     ProfScope ps(ctx, "pack_a");
@@ -583,13 +588,10 @@ static fmmt_status build_plans(fmmt_op* op) {
   free_workspace(op);
   op->descs.clear();
   op->batches.clear();
-  for (auto b : op->bpk_static)
-    if (b) cudaFree(b);
+  for (auto& b : op->bpk_static) dev_free(op, b);
   op->bpk_static.clear();
-  if (op->Mpk) cudaFree(op->Mpk);
-  op->Mpk = nullptr;
+  dev_free(op, op->Mpk);
   op->mpk_floats = 0;
-  op->packb_bytes = 0;
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
   if (op->PB <= 0) {
     // batch size: the per-batch intermediates L2-resident (48 MB) ...
@@ -671,19 +673,14 @@ static fmmt_status build_plans(fmmt_op* op) {
         dg.Ap = op->E_pk;
         dg.a_nkc = (int)((r34 + fmmt::TC_BK - 1) / fmmt::TC_BK);
         float* mpk = nullptr;
-        if (dg.Ap && op->ctx->pack_b && op->ctx->gemm_impl == 1 && !op->ctx->warp_specialised) {
+        if (dg.Ap && op->ctx->pack_b && op->ctx->gemm_impl == 1) {
           // M_q changes every batch: pre-split it into Mpk right before the G GEMM (sized for the largest batch)
           const int64_t need = packb_floats(dg);
           if (op->mpk_floats < need) {
-            if (op->Mpk) cudaFree(op->Mpk);
-            op->Mpk = nullptr;
+            dev_free(op, op->Mpk);
             op->mpk_floats = 0;
-            if (cudaMalloc(&op->Mpk, need * sizeof(float)) != cudaSuccess) {
-              cudaGetLastError();
-              return set_err(op->ctx, FMMT_E_NOMEM, "pre-split M allocation (%lld B) failed", (long long)(need * 4));
-            }
+            if ((st = dev_alloc(op, &op->Mpk, need * 4, MEM_WORKSPACE, "pre-split M"))) return st;
             op->mpk_floats = need;
-            op->packb_bytes += need * 4;
           }
           mpk = op->Mpk;
           dg.Bp = mpk;
@@ -720,14 +717,14 @@ static fmmt_status build_plans(fmmt_op* op) {
     op->batches.push_back(b);
   }
   if (op->zscr) {   // batch size may have changed
-    cudaFree(op->zscr);
-    op->zscr = nullptr;
+    dev_free(op, op->zscr);
     op->zscr_elems = 0;
   }
   if ((st = ensure_zscr(op))) return st;
   FMMT_CUDA(op->ctx, cudaStreamSynchronize(op->ctx->stream));   // static pre-splits done
   if (!op->descs.empty()) {
-    FMMT_CUDA(op->ctx, cudaMalloc(&op->d_descs, op->descs.size() * sizeof(GemmDesc)));
+    if ((st = dev_alloc(op, &op->d_descs, (int64_t)(op->descs.size() * sizeof(GemmDesc)), MEM_WORKSPACE, "descriptors")))
+      return st;
     FMMT_CUDA(op->ctx, cudaMemcpy(op->d_descs, op->descs.data(), op->descs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
   }
   return FMMT_OK;
@@ -737,18 +734,7 @@ static fmmt_status build_plans(fmmt_op* op) {
 constexpr int TC_G = 1;   // thread groups per tensor-core CTA (2 = 256 threads: measured slower)
 
 template <int BN>
-static fmmt_status launch_tcw_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
-  constexpr int SMEM = fmmt::TcwCfg<BN>::SMEM;
-  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_cgemm<BN>, SMEM));
-  const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));   // 1 CTA / SM
-  fmmt::k_tcw_cgemm<BN><<<grid, 256, SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, (int)total);
-  return FMMT_OK;
-}
-
-template <int BN>
 static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
-  if (ctx->warp_specialised) return launch_tcw_bn<BN>(ctx, L, d);
   using Cfg = fmmt::TcGemmCfg<BN, TC_G>;
   FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN, TC_G>, Cfg::SMEM));
   const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
@@ -759,28 +745,12 @@ static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDe
   return FMMT_OK;
 }
 
-template <int BN, int SPLIT = 0>
-static fmmt_status launch_tc1_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
-  using Cfg = fmmt::v1::TcGemmCfg<BN>;
-  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::v1::k_tc_cgemm<BN, SPLIT>, Cfg::SMEM));
-  dim3 grid((unsigned)L.tc_maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
-  fmmt::v1::k_tc_cgemm<BN, SPLIT><<<grid, 128, Cfg::SMEM, ctx->stream>>>(d);
-  return FMMT_OK;
-}
-
 // Launch one descriptor group.  impl: 0 = FP32 FFMA kernel, 1 = tcgen05 3xTF32
-// (cp.async into the UMMA layout, 2 MMAs per K-step), 2 = first tcgen05 design (A/B).
+// (cp.async / bulk copies into the UMMA layout, 2 MMAs per K-step).
 static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d_descs, int impl) {
   if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
   fmmt_status st = FMMT_OK;
-  if (impl == 3 || impl == 4) {   // split experiments (test hook only)
-    if (impl == 3) st = launch_tc1_bn<64, 1>(ctx, L, d_descs + L.first);
-    else st = launch_tc1_bn<64, 2>(ctx, L, d_descs + L.first);
-  } else if (impl == 2) {
-    if (L.tc_bn == 64) st = launch_tc1_bn<64>(ctx, L, d_descs + L.first);
-    else if (L.tc_bn == 32) st = launch_tc1_bn<32>(ctx, L, d_descs + L.first);
-    else st = launch_tc1_bn<16>(ctx, L, d_descs + L.first);
-  } else if (impl == 1) {
+  if (impl == 1) {
     if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, L, d_descs + L.first);
     else st = launch_tc_bn<16>(ctx, L, d_descs + L.first);
   } else {
@@ -915,46 +885,16 @@ static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& 
   return FMMT_OK;
 }
 
-template <int N3>
-static fmmt_status launch_tcw_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  constexpr int SMEM = fmmt::TcwCfg<(N3 < 16 ? 16 : N3)>::SMEM;
-  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, ctx->num_sms));
-  if (mode == fmmt::Z_RESTORE) {
-    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_conv_z<N3, fmmt::Z_RESTORE>, SMEM));
-    fmmt::k_tcw_conv_z<N3, fmmt::Z_RESTORE><<<grid, 256, SMEM, ctx->stream>>>(a, nq);
-  } else {
-    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tcw_conv_z<N3, fmmt::Z_LOWRANK>, SMEM));
-    fmmt::k_tcw_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 256, SMEM, ctx->stream>>>(a, nq);
-  }
-  FMMT_CUDA(ctx, cudaGetLastError());
-  return FMMT_OK;
-}
-
 // Directions per z tile: > 1 only when all directions share G (TT-4D's T1) and the
 // V_q of consecutive directions are contiguous ([q][kz][c]), up to 2 n3 = 64 columns.
 template <int N3>
 static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  if (ctx->warp_specialised) return launch_tcw_z<N3>(ctx, mode, nq, a);
   const bool shareable = a.g_stride == 0 && !a.v_off && a.v_stride == (int64_t)N3 * a.v_sk && mode != fmmt::Z_RESTORE;
   if (shareable && N3 <= 32 && ctx->z_multidir) {
     constexpr int ND = 64 / N3 > 4 ? 4 : 64 / N3;
     return launch_tc_z_nd<N3, ND>(ctx, mode, nq, a);
   }
   return launch_tc_z_nd<N3, 1>(ctx, mode, nq, a);
-}
-
-template <int N3>
-static fmmt_status launch_tc1_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  using Cfg = fmmt::v1::TcGemmCfg<(N3 < 16 ? 16 : N3)>;
-  const void* fn = mode == fmmt::Z_RESTORE ? (const void*)fmmt::v1::k_tc_conv_z<N3, fmmt::Z_RESTORE>
-                                           : (const void*)fmmt::v1::k_tc_conv_z<N3, fmmt::Z_LOWRANK>;
-  FMMT_CUDA(ctx, set_smem_once(fn, Cfg::SMEM));
-  dim3 grid((unsigned)((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM), (unsigned)nq);
-  if (mode == fmmt::Z_RESTORE) fmmt::v1::k_tc_conv_z<N3, fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
-  else fmmt::v1::k_tc_conv_z<N3, fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a);
-  FMMT_CUDA(ctx, cudaGetLastError());
-  return FMMT_OK;
 }
 
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0,
@@ -1005,7 +945,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     FMMT_CUDA(ctx, cudaGetLastError());
     return FMMT_OK;
   }
-  if (ctx->gemm_impl >= 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
+  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
     fill_zargs(op, a);
     a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
@@ -1016,22 +956,13 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
     a.Tout = Tout;
     // TT-4D: A (T1) is pre-split once per op; pre-split this batch's V_q too, so the z-stage streams
     // both operands with bulk copies and no per-thread conversion (FMMT_PACKB=0 disables)
-    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b && ctx->gemm_impl == 1 && !ctx->warp_specialised &&
-        !ctx->z_multidir) {
+    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b && !ctx->z_multidir) {
       fmmt_status st = pack_v(op, a, nq);
       if (st) return st;
     }
     static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
                                    "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
-    if (ctx->gemm_impl == 2) {
-      switch (op->n3) {
-        case 4: return launch_tc1_z<4>(ctx, mode, nq, a);
-        case 8: return launch_tc1_z<8>(ctx, mode, nq, a);
-        case 16: return launch_tc1_z<16>(ctx, mode, nq, a);
-        default: return launch_tc1_z<32>(ctx, mode, nq, a);
-      }
-    }
     switch (op->n3) {
       case 4: return launch_tc_z<4>(ctx, mode, nq, a);
       case 8: return launch_tc_z<8>(ctx, mode, nq, a);
@@ -1073,9 +1004,7 @@ static fmmt_status ensure_zscr(fmmt_op* op) {
   const int64_t need = op->PB * op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2;
   if (op->zscr && op->zscr_elems >= need) return FMMT_OK;
   if (op->zscr) {
-    cudaFree(op->zscr);
-    op->ws_bytes -= op->zscr_elems * 8;
-    op->zscr = nullptr;
+    dev_free(op, op->zscr);
   }
   fmmt_status st = cmalloc(op, &op->zscr, need);
   if (!st) op->zscr_elems = need;
@@ -1093,20 +1022,11 @@ static fmmt_status ensure_vpk(fmmt_op* op) {
   const int64_t tiles_n = op->n3 == 64 ? 2 : (op->n3 + BN - 1) / BN;   // n3 = 64: one 32-column pack per parity pass
   const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK);   // BP_FLOATS = 2 NR x 2 BK, NR = 2 BN
   if (op->vpk_floats >= need) return FMMT_OK;
-  cudaStreamSynchronize(ctx->stream);
-  for (auto& g : op->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  op->graphs.clear();
-  if (op->Vpk) {
-    cudaFree(op->Vpk);
-    op->ws_bytes -= op->vpk_floats * 4;
-  }
-  op->Vpk = nullptr;
+  drop_graphs(op);
+  dev_free(op, op->Vpk);
   op->vpk_floats = 0;
-  cudaError_t e = cudaMalloc(&op->Vpk, need * sizeof(float));
-  if (e != cudaSuccess) return set_err(ctx, FMMT_E_NOMEM, "pre-split V workspace: %s", cudaGetErrorString(e));
+  if (fmmt_status st = dev_alloc(op, &op->Vpk, need * 4, MEM_WORKSPACE, "pre-split V workspace")) return st;
   op->vpk_floats = need;
-  op->ws_bytes += need * 4;
   return FMMT_OK;
 }
 
@@ -1114,17 +1034,9 @@ static fmmt_status ensure_vpk(fmmt_op* op) {
 static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
   if (fmmt_status st = ensure_vpk(op)) return st;
   if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
-  fmmt_ctx* ctx = op->ctx;
-  cudaStreamSynchronize(ctx->stream);
-  for (auto& g : op->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  op->graphs.clear();
+  drop_graphs(op);
   const int64_t elems = op->ndir * (op->n3 / 2) * op->n1 * op->n2;
-  if (op->W) {
-    cudaFree(op->W);
-    op->ws_bytes -= op->w_ncomp * elems * 8;
-    op->W = nullptr;
-  }
+  dev_free(op, op->W);
   op->w_ncomp = std::max<int64_t>(ncomp, op->w_ncomp);
   fmmt_status st = cmalloc(op, &op->W, op->w_ncomp * elems);
   if (st) return st;
@@ -1155,6 +1067,7 @@ static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void*
                                         int64_t Ny, int64_t Nz, int64_t ncomp = 1) {
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
+  if (!op->translatable) return set_err(ctx, FMMT_E_UNSUPPORTED, "storage-only op (shape outside the translate path)");
   CHECK_ARG(ctx, in && out, "null signature pointer");
   CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
   CHECK_SHAPE(ctx, 2 * Nx == op->n1 && 2 * Ny == op->n2 && 2 * Nz == op->n3, "grid %lldx%lldx%lld does not match op n=%lldx%lldx%lld",
@@ -1182,10 +1095,16 @@ static fmmt_status check_translate_args(fmmt_op* op, const void* in, const void*
 // cudaGraphLaunch (the hot path is otherwise bound by ~300 host-side kernel
 // launches per matvec).  Direct launches when profiling (per-kernel events) or
 // on the legacy default stream (not capturable).
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <class F>
 static fmmt_status run_graphed(fmmt_op* op, const void* k0, const void* k1, const void* k2, const void* k3, int64_t k4,
                                F&& body, const void* k5 = nullptr) {
   fmmt_ctx* ctx = op->ctx;
+  NvtxRange nr("fmmt_matvec");
   if (ctx->stream == nullptr || !ctx->use_graphs) return body();
   if (ctx->profiling) {
     // per-kernel profile: capture the matvec with its event-record nodes and run it as one
@@ -1286,7 +1205,6 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_AGG_STAGED")) ctx->agg_staged = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
-  if (const char* e = getenv("FMMT_WS")) ctx->warp_specialised = atoi(e) != 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
     ncclUniqueId id;
@@ -1365,7 +1283,7 @@ fmmt_status fmmt_prof_read(fmmt_ctx* ctx, const char** names, double* ms, int64_
 int64_t fmmt_launch_count(const fmmt_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl) {
-  if (!ctx || impl < 0 || impl > 2) return FMMT_E_ARG;
+  if (!ctx || impl < 0 || impl > 1) return FMMT_E_ARG;
   ctx->gemm_impl = impl;
   return FMMT_OK;
 }
@@ -1373,7 +1291,7 @@ fmmt_status fmmt_set_gemm_impl(fmmt_ctx* ctx, int impl) {
 fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64_t k, int transA, int transB,
                             const fmmt_c64* A, int64_t lda, const fmmt_c64* B, int64_t ldb, fmmt_c64* C, int64_t ldc) {
   if (!ctx) return FMMT_E_ARG;
-  CHECK_ARG(ctx, impl >= 0 && impl <= 4, "impl must be 0..4");
+  CHECK_ARG(ctx, impl >= 0 && impl <= 1, "impl must be 0 (FFMA) or 1 (tcgen05)");
   CHECK_ARG(ctx, A && B && C, "null matrix");
   CHECK_SHAPE(ctx, m >= 1 && n >= 1 && k >= 1 && m < (1 << 30) && n < (1 << 30) && k < (1 << 30), "bad gemm dims");
   cudaSetDevice(ctx->device);
@@ -1385,7 +1303,7 @@ fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64
 
 fmmt_status fmmt_op_import(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
                            const int64_t* ranks, const fmmt_c64* const* arrays, int64_t narrays, fmmt_op** op) {
-  return fmmt_internal::create_op(ctx, format, n1, n2, n3, ndir, ranks, (const void* const*)arrays, narrays, op);
+  return fmmt_internal::create_op(ctx, format, n1, n2, n3, ndir, ranks, (const void* const*)arrays, narrays, op, false);
 }
 
 fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
@@ -1411,8 +1329,9 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
   for (auto e : op->arr_elems) comp += e;
   info->compressed_bytes = comp * 8;
   info->original_bytes = op->n1 * op->n2 * op->n3 * op->ndir * 8;
-  info->workspace_bytes = op->ws_bytes + (op->tbar1 ? op->n1 * op->n2 * rk(op, 0, 1) * 8 : 0) +
-                          (op->E ? op->n1 * op->n2 * rk(op, 0, 5) * 8 : 0) + op->pack_bytes + op->packb_bytes;
+  // everything else the op holds on the device: derived / pre-split operands (T1, E, packed factors) and
+  // the matvec workspaces (mem registry; compressed_bytes counts the factors alone)
+  info->workspace_bytes = mem_bytes(op, MEM_DERIVED) + mem_bytes(op, MEM_WORKSPACE);
   info->batch = op->PB;
   // restore complex MACs per matvec (a3 + a4), in the contraction order the kernels use
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n = n1 * n2 * n3;
@@ -1445,6 +1364,21 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info) {
     }
   }
   info->restore_cmac = cm;
+  info->translatable = op->translatable ? 1 : 0;
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_op_export(const fmmt_op* op, int64_t index, fmmt_c64* dst, int64_t cap, int64_t* count) {
+  if (!op || !count) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, index >= 0 && index < (int64_t)op->arr.size(), "array index %lld not in [0, %lld)", (long long)index,
+            (long long)op->arr.size());
+  *count = op->arr_elems[index];
+  if (!dst) return FMMT_OK;
+  CHECK_ARG(ctx, cap >= *count, "export buffer too small (%lld < %lld)", (long long)cap, (long long)*count);
+  cudaSetDevice(ctx->device);
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  FMMT_CUDA(ctx, cudaMemcpy(dst, op->arr[index], *count * sizeof(float2), cudaMemcpyDefault));
   return FMMT_OK;
 }
 
@@ -1460,12 +1394,10 @@ fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_
 
 fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs) {
   if (!op || dirs < 0) return FMMT_E_ARG;
+  if (!op->translatable) return set_err(op->ctx, FMMT_E_UNSUPPORTED, "storage-only op");
   cudaSetDevice(op->ctx->device);
-  cudaStreamSynchronize(op->ctx->stream);
+  drop_graphs(op);
   op->PB = std::min<int64_t>(dirs, op->ndir);
-  for (auto& g : op->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  op->graphs.clear();
   return build_plans(op);
 }
 
@@ -1491,24 +1423,32 @@ fmmt_status fmmt_translate_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* 
 static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float* w, float2* sum_out, int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
   const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2) * ncomp;   // [comp][Nz][Ny][Nx] per direction
-  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(op->ndir, std::max<int64_t>(1, (148 * 8 * 128) / std::max<int64_t>(K, 1))));
-  if (!op->partial || op->nsplit < nsplit || op->partial_elems < (int64_t)nsplit * K) {
-    if (op->partial) cudaFree(op->partial);
-    op->partial = nullptr;
+  // direction splits: enough (K x nsplit) threads to fill the GPU, at most 64 (k_dirsum_final: a warp per output)
+  const int nsplit = (int)std::max<int64_t>(
+      1, std::min<int64_t>(std::min<int64_t>(op->ndir, 64), (int64_t)ctx->num_sms * 1024 / std::max<int64_t>(K, 1)));
+  if (nsplit > 1 && (!op->partial || op->partial_elems < (int64_t)nsplit * K)) {
+    // captured matvec graphs hold the old buffer: drop them first (this call is never captured: a new
+    // graph key always runs once directly before it is captured, see run_graphed)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return set_err(ctx, FMMT_E_STATE, "direction-sum workspace grows during capture");
+    drop_graphs(op);
+    dev_free(op, op->partial);
+    op->partial_elems = 0;
     fmmt_status st = cmalloc(op, &op->partial, (int64_t)nsplit * K);
     if (st) return st;
-    op->nsplit = nsplit;
     op->partial_elems = (int64_t)nsplit * K;
   }
   {
     ProfScope ps(ctx, "dirsum_partial");
     dim3 grid((unsigned)((K + 127) / 128), (unsigned)nsplit);
-    fmmt::k_dirsum_partial<<<grid, 128, 0, ctx->stream>>>(sig, w, op->partial, K, (int)op->ndir, nsplit);
+    fmmt::k_dirsum_partial<<<grid, 128, 0, ctx->stream>>>(sig, w, nsplit > 1 ? op->partial : sum_out, K, (int)op->ndir,
+                                                           nsplit);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
-  {
+  if (nsplit > 1) {
     ProfScope ps(ctx, "dirsum_final");
-    fmmt::k_dirsum_final<<<(unsigned)((K + 127) / 128), 128, 0, ctx->stream>>>(op->partial, sum_out, K, nsplit);
+    fmmt::k_dirsum_final<<<(unsigned)((K + 7) / 8), 256, 0, ctx->stream>>>(op->partial, sum_out, K, nsplit);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
   if (ctx->world > 1) {
@@ -1528,8 +1468,8 @@ fmmt_status fmmt_translate_sum_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c
   if (!sig_out) {
     const int64_t need = op->ndir * ncomp * (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
     if (!op->sigtmp || op->sigtmp_elems < need) {
-      if (op->sigtmp) cudaFree(op->sigtmp);
-      op->sigtmp = nullptr;
+      drop_graphs(op);
+      dev_free(op, op->sigtmp);
       fmmt_status st = cmalloc(op, &op->sigtmp, need);
       if (st) return st;
       op->sigtmp_elems = need;
@@ -1557,13 +1497,19 @@ fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, co
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
   CHECK_ARG(ctx, sig_in_host && w_host && sum_out_host, "null host pointer");
-  CHECK_SHAPE(ctx, ndir == op->ndir, "ndir mismatch");
+  if (!op->translatable) return set_err(ctx, FMMT_E_UNSUPPORTED, "storage-only op");
+  CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
+  // shape first: the staging buffers are sized from the op, never from the caller's arguments
+  CHECK_SHAPE(ctx, 2 * Nx == op->n1 && 2 * Ny == op->n2 && 2 * Nz == op->n3, "grid %lldx%lldx%lld does not match op n=%lldx%lldx%lld",
+              (long long)Nx, (long long)Ny, (long long)Nz, (long long)op->n1, (long long)op->n2, (long long)op->n3);
   cudaSetDevice(ctx->device);
-  const int64_t K = Nx * Ny * Nz;
+  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
   if (!op->d_in_host) {
-    FMMT_CUDA(ctx, cudaMalloc(&op->d_in_host, ndir * K * sizeof(float2)));
-    FMMT_CUDA(ctx, cudaMalloc(&op->d_w_host, ndir * sizeof(float)));
-    FMMT_CUDA(ctx, cudaMalloc(&op->d_sum_host, K * sizeof(float2)));
+    fmmt_status st;
+    if ((st = dev_alloc(op, &op->d_in_host, op->ndir * K * 8, MEM_WORKSPACE, "host staging")) ||
+        (st = dev_alloc(op, &op->d_w_host, op->ndir * 4, MEM_WORKSPACE, "host staging")) ||
+        (st = dev_alloc(op, &op->d_sum_host, K * 8, MEM_WORKSPACE, "host staging")))
+      return st;
   }
   FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_in_host, sig_in_host, ndir * K * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
   FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_w_host, w_host, ndir * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
@@ -1711,6 +1657,7 @@ fmmt_status fmmt_far_matvec(fmmt_op* op, const fmmt_c64* P, const fmmt_c64* I, c
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
   CHECK_ARG(ctx, I && w && y, "null pointer");
+  if (!op->translatable) return set_err(ctx, FMMT_E_UNSUPPORTED, "storage-only op");
   fmmt_status st = check_agg_args(ctx, P, box_ptr, ndir, N, ncomp, Nx, Ny, Nz);
   if (st) return st;
   CHECK_SHAPE(ctx, ndir == op->ndir, "ndir %lld != op ndir %lld", (long long)ndir, (long long)op->ndir);
@@ -1719,14 +1666,8 @@ fmmt_status fmmt_far_matvec(fmmt_op* op, const fmmt_c64* P, const fmmt_c64* I, c
   const int64_t K = Nx * Ny * Nz, elems = ndir * ncomp * K;
   const int64_t pelems = std::max<int64_t>(1, (int64_t)agg_nsplit(ctx, ndir, K) * N);
   if (op->fAB_elems < elems || op->fPart_elems < pelems) {   // workspaces change: drop captured graphs
-    cudaStreamSynchronize(ctx->stream);
-    for (auto& g : op->graphs)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    op->graphs.clear();
-    op->ws_bytes -= (2 * op->fAB_elems + op->fPart_elems) * 8;
-    for (float2** b : {&op->fA, &op->fB, &op->fPart})
-      if (*b) cudaFree(*b);
-    op->fA = op->fB = op->fPart = nullptr;
+    drop_graphs(op);
+    for (float2** b : {&op->fA, &op->fB, &op->fPart}) dev_free(op, *b);
     op->fAB_elems = op->fPart_elems = 0;
     if ((st = cmalloc(op, &op->fA, elems)) || (st = cmalloc(op, &op->fB, elems)) || (st = cmalloc(op, &op->fPart, pelems)))
       return st;
@@ -1750,6 +1691,7 @@ fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
   if (!op) return FMMT_E_ARG;
   fmmt_ctx* ctx = op->ctx;
   CHECK_ARG(ctx, T_p, "null output");
+  if (!op->translatable) return set_err(ctx, FMMT_E_UNSUPPORTED, "storage-only op (shape outside the translate path)");
   CHECK_ARG(ctx, p >= 0 && p < op->ndir, "direction %lld out of range", (long long)p);
   cudaSetDevice(ctx->device);
   const int64_t n = op->n1 * op->n2 * op->n3;
@@ -1774,15 +1716,24 @@ fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
 namespace fmmt_internal {
 
 fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
-                      const int64_t* ranks, const void* const* arrays, int64_t narrays, fmmt_op** out) {
+                      const int64_t* ranks, const void* const* arrays, int64_t narrays, fmmt_op** out,
+                      bool storage_only_ok) {
   if (!ctx || !out) return FMMT_E_ARG;
   *out = nullptr;
   CHECK_ARG(ctx, format >= FMMT_DENSE && format <= FMMT_TT4D, "bad format %d", (int)format);
   CHECK_ARG(ctx, arrays != nullptr, "null arrays");
   CHECK_SHAPE(ctx, n1 >= 2 && n2 >= 2 && n3 >= 2 && ndir >= 1, "bad dims");
   CHECK_SHAPE(ctx, n1 % 2 == 0 && n2 % 2 == 0 && n3 % 2 == 0, "n must be even (n = 2N)");
-  if (!(is_pow2(n1) && is_pow2(n2) && is_pow2(n3) && n1 >= 4 && n2 >= 4 && n3 >= 4 && n1 <= 256 && n2 <= 256 && n3 <= 64))
-    return set_err(ctx, FMMT_E_UNSUPPORTED, "translate path supports power-of-two n1,n2 in [4,256], n3 in [4,64]; got %lldx%lldx%lld",
+  bool translatable = is_pow2(n1) && is_pow2(n2) && is_pow2(n3) && n1 >= 4 && n2 >= 4 && n3 >= 4 && n1 <= 256 &&
+                      n2 <= 256 && n3 <= 64;
+  if (translatable) {   // the xy FFT kernel holds one padded plane (plus twiddles) in shared memory
+    const XYKernels xk = get_xy((int)n1, (int)n2);
+    translatable = xk.fwd && (int64_t)(FMMT_TW_NMAX + xk.plane_smem) * 8 <= 227 * 1024;
+  }
+  if (!translatable && !storage_only_ok)
+    return set_err(ctx, FMMT_E_UNSUPPORTED,
+                   "translate path supports power-of-two n1,n2 in [4,256] (one xy plane <= 227 KB of shared memory), "
+                   "n3 in [4,64]; got %lldx%lldx%lld",
                    (long long)n1, (long long)n2, (long long)n3);
   static const int nslots_of[] = {0, 3, 4, 6, 2, 3};
   static const int narr_of[] = {1, 4, 5, 7, 3, 4};
@@ -1794,6 +1745,7 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
   op->format = format;
   op->n1 = n1; op->n2 = n2; op->n3 = n3; op->ndir = ndir;
   op->nslots = nslots_of[format];
+  op->translatable = translatable;
   const bool per_dir = format == FMMT_TUCKER3D || format == FMMT_TT3D;
   if (op->nslots) {
     CHECK_ARG(ctx, ranks != nullptr, "null ranks");
@@ -1857,13 +1809,12 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
   op->arr_elems = elems;
   for (size_t i = 0; i < elems.size(); ++i) {
     float2* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, std::max<int64_t>(1, elems[i]) * sizeof(float2));
-    if (e != cudaSuccess) {
+    if (fmmt_status st = dev_alloc(op, &d, std::max<int64_t>(1, elems[i]) * 8, MEM_FACTOR, "factor")) {
       fmmt_op_destroy(op);
-      return set_err(ctx, FMMT_E_NOMEM, "factor allocation failed: %s", cudaGetErrorString(e));
+      return st;
     }
     op->arr.push_back(d);
-    e = cudaMemcpy(d, arrays[i], elems[i] * sizeof(float2), cudaMemcpyDefault);
+    cudaError_t e = cudaMemcpy(d, arrays[i], elems[i] * sizeof(float2), cudaMemcpyDefault);
     if (e != cudaSuccess) {
       fmmt_op_destroy(op);
       return set_err(ctx, FMMT_E_CUDA, "factor copy failed: %s", cudaGetErrorString(e));
@@ -1878,19 +1829,30 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
       voff[p] = op->off[vi][p];
       rz[p] = (int)(format == FMMT_TUCKER3D ? R(p, 2) : R(p, 1));
     }
-    cudaMalloc(&op->d_voff, ndir * sizeof(int64_t));
-    cudaMalloc(&op->d_rank, ndir * sizeof(int));
-    cudaMemcpy(op->d_voff, voff.data(), ndir * sizeof(int64_t), cudaMemcpyHostToDevice);
-    cudaMemcpy(op->d_rank, rz.data(), ndir * sizeof(int), cudaMemcpyHostToDevice);
+    fmmt_status st;
+    if ((st = dev_alloc(op, &op->d_voff, ndir * 8, MEM_DERIVED, "z-stage offsets")) ||
+        (st = dev_alloc(op, &op->d_rank, ndir * 4, MEM_DERIVED, "z-stage ranks"))) {
+      fmmt_op_destroy(op);
+      return st;
+    }
+    cudaError_t e1 = cudaMemcpy(op->d_voff, voff.data(), ndir * sizeof(int64_t), cudaMemcpyHostToDevice);
+    cudaError_t e2 = cudaMemcpy(op->d_rank, rz.data(), ndir * sizeof(int), cudaMemcpyHostToDevice);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      fmmt_op_destroy(op);
+      return set_err(ctx, FMMT_E_CUDA, "z-stage table copy failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    }
+  }
+  if (!translatable) {   // storage-only: factors, ranks, info and export (no plans, no derived operands)
+    *out = op;
+    return FMMT_OK;
   }
   if (format == FMMT_HTUCKER4D) {
     // Direction-independent part of Fig. 3(c), once per op, in FP64 (setup):
     //   E[i + n1 jj + n12 j] = sum_{a,b} U1[i,a] U2[jj,b] (C12 . C1234)[a + r1 b, j]
     const int64_t r1 = R(0, 0), r2 = R(0, 1), r12 = R(0, 4), r34 = R(0, 5), n12 = n1 * n2;
-    if (cudaMalloc(&op->E, n12 * r34 * sizeof(float2)) != cudaSuccess) {
-      cudaGetLastError();
+    if (fmmt_status ast = dev_alloc(op, &op->E, n12 * r34 * 8, MEM_DERIVED, "H-Tucker E")) {
       fmmt_op_destroy(op);
-      return set_err(ctx, FMMT_E_NOMEM, "H-Tucker E allocation failed");
+      return ast;
     }
     fmmt_status st = fmmt_internal::htucker_E_fp64(ctx, op->arr[0], op->arr[1], op->arr[4], op->arr[6], n1, n2, r1, r2,
                                                    r12, r34, op->E);
@@ -1912,10 +1874,9 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
   if (format == FMMT_TT4D) {
     // T1 = U1 . C1 (Fig. 4(a) step 1, reused by every direction of Fig. 4(b)), stored [b][ij], in FP64
     const int64_t r1 = R(0, 0), r2 = R(0, 1);
-    if (cudaMalloc(&op->tbar1, n1 * n2 * r2 * sizeof(float2)) != cudaSuccess) {
-      cudaGetLastError();
+    if (fmmt_status ast = dev_alloc(op, &op->tbar1, n1 * n2 * r2 * 8, MEM_DERIVED, "TT-4D T1")) {
       fmmt_op_destroy(op);
-      return set_err(ctx, FMMT_E_NOMEM, "T1 allocation failed");
+      return ast;
     }
     fmmt_status tst = fmmt_internal::tt4d_T1_fp64(ctx, op->arr[0], op->arr[1], n1, r1, n2, r2, op->tbar1);
     if (tst) {

@@ -32,7 +32,6 @@ struct fmmt_ctx {
   bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)
   int tc_ctas_per_sm = 2;           // tensor-core GEMM grid: CTAs per SM = the resident count (each loops over tiles)
   int tc_ctas_z = 4;                // tensor-core z-stage grid: CTAs per SM (two waves measured faster there)
-  bool warp_specialised = false;    // tensor-core kernels: producer / consumer warps, 1 CTA/SM (FMMT_WS)
   bool agg_staged = true;           // aggregation: shared-memory staged kernel (FMMT_AGG_STAGED=0: warp-per-box)
   void* agg_part = nullptr;         // disaggregation partial sums [nsplit][N] (complex64)
   int64_t agg_part_elems = 0;
@@ -48,10 +47,12 @@ namespace fmmt_internal {
 
 fmmt_status set_err(fmmt_ctx* ctx, fmmt_status st, const char* fmt, ...);
 
-// Create an op from complex64 arrays (host or device memory, copied).
+// Create an op from complex64 arrays (host or device memory, copied).  storage_only_ok: shapes
+// outside the translate path give a storage-only op (ranks / info / export; translate and restore
+// return FMMT_E_UNSUPPORTED) instead of an error (the compressor's paper-sweep sizes).
 fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3,
                       int64_t ndir, const int64_t* ranks, const void* const* arrays,
-                      int64_t narrays, fmmt_op** out);
+                      int64_t narrays, fmmt_op** out, bool storage_only_ok);
 
 void setup_release(fmmt_ctx* ctx);   // free cuBLAS / cuSOLVER handles
 

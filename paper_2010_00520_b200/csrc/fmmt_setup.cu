@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -632,20 +633,108 @@ static fmmt_status to_c64(Setup& S, const double2* a, int64_t n, float2* dst) {
   return FMMT_OK;
 }
 
-extern "C" fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
-                                     int64_t dir_begin, int64_t dir_count, fmmt_format format, double tol, fmmt_op** op) {
+// ---------------------------------------------------------------- sharded 4D setup (NCCL broadcast)
+// Element counts of a 4D format's arrays (import order) for `rows` direction-factor rows, and which
+// array is the direction factor (rows x r, column-major) with its rank slot.
+static std::vector<int64_t> arrays4d(fmmt_format f, int64_t n1, int64_t n2, int64_t n3, int64_t rows, const int64_t* r,
+                                     int* dir_arr) {
+  switch (f) {
+    case FMMT_TUCKER4D: *dir_arr = 4; return {r[0] * r[1] * r[2] * r[3], n1 * r[0], n2 * r[1], n3 * r[2], rows * r[3]};
+    case FMMT_HTUCKER4D:
+      *dir_arr = 3;
+      return {n1 * r[0], n2 * r[1], n3 * r[2], rows * r[3], r[0] * r[1] * r[4], r[2] * r[3] * r[5], r[4] * r[5]};
+    default: *dir_arr = 3; return {n1 * r[0], r[0] * n2 * r[1], r[1] * n3 * r[2], rows * r[2]};
+  }
+}
+static int dir_rank_slot(fmmt_format f) { return f == FMMT_TT4D ? 2 : 3; }
+
+// Broadcast ranks + all arrays (every direction row) from rank 0 over the context's communicator, then
+// keep rows [b, b + c) of the direction factor and create the local op.  `full` (root only) are the arrays
+// with all ndir rows; receivers pass an empty vector and get them.
+static fmmt_status bcast_and_create(fmmt_ctx* ctx, int64_t n1, int64_t n2, int64_t n3, int64_t ndir, int64_t b, int64_t c,
+                                    fmmt_format format, std::vector<int64_t> ranks, std::vector<const void*> full,
+                                    fmmt_op** op) {
+  ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
+  if (!comm) return set_err(ctx, FMMT_E_STATE, "sharded compress needs a communicator (fmmt_init_sharded)");
+  const bool root = ctx->rank == 0;
+  // 1. ranks (6 int64 slots)
+  DBuf hdr;
+  SETUP_TRY(dalloc(ctx, hdr, 6 * 8));
+  int64_t h[6] = {0, 0, 0, 0, 0, 0};
+  if (root)
+    for (size_t i = 0; i < ranks.size() && i < 6; ++i) h[i] = ranks[i];
+  FMMT_CUDA(ctx, cudaMemcpyAsync(hdr.p, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+  ncclResult_t nr = ncclBroadcast(hdr.p, hdr.p, 6, ncclInt64, 0, comm, ctx->stream);
+  if (nr != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclBroadcast(ranks): %s", ncclGetErrorString(nr));
+  FMMT_CUDA(ctx, cudaMemcpyAsync(h, hdr.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  static const int nslots_of[] = {0, 3, 4, 6, 2, 3};
+  ranks.assign(h, h + nslots_of[format]);
+  for (auto r : ranks)
+    if (r < 1) return set_err(ctx, FMMT_E_STATE, "broadcast ranks invalid (root failed?)");
+  // 2. one payload buffer holding every array back to back (complex64)
+  int dir_arr = 0;
+  const std::vector<int64_t> el = arrays4d(format, n1, n2, n3, ndir, ranks.data(), &dir_arr);
+  std::vector<int64_t> off(el.size() + 1, 0);
+  for (size_t i = 0; i < el.size(); ++i) off[i + 1] = off[i] + el[i];
+  DBuf pay;
+  SETUP_TRY(dalloc(ctx, pay, off.back() * 8));
+  float2* P = pay.as<float2>();
+  if (root)
+    for (size_t i = 0; i < el.size(); ++i)
+      FMMT_CUDA(ctx, cudaMemcpyAsync(P + off[i], full[i], el[i] * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  // (2 floats per complex; NCCL counts are size_t)
+  nr = ncclBroadcast(P, P, (size_t)(2 * off.back()), ncclFloat, 0, comm, ctx->stream);
+  if (nr != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclBroadcast(factors): %s", ncclGetErrorString(nr));
+  // 3. this rank's direction rows
+  const int64_t r = ranks[dir_rank_slot(format)];
+  DBuf loc;
+  SETUP_TRY(dalloc(ctx, loc, c * r * 8));
+  FMMT_CUDA(ctx, cudaMemcpy2DAsync(loc.p, c * 8, P + off[dir_arr] + b, ndir * 8, c * 8, r, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<const void*> arrs;
+  for (size_t i = 0; i < el.size(); ++i) arrs.push_back((int)i == dir_arr ? loc.p : (const void*)(P + off[i]));
+  return fmmt_internal::create_op(ctx, format, n1, n2, n3, c, ranks.data(), arrs.data(), (int64_t)arrs.size(), op, true);
+}
+
+static fmmt_status compress_receive(fmmt_ctx* ctx, int64_t n1, int64_t n2, int64_t n3, int64_t ndir, int64_t b, int64_t c,
+                                    fmmt_format format, fmmt_op** op) {
+  return bcast_and_create(ctx, n1, n2, n3, ndir, b, c, format, {}, {}, op);
+}
+
+static fmmt_status compress_send(fmmt_ctx* ctx, int64_t n1, int64_t n2, int64_t n3, int64_t ndir, int64_t b, int64_t c,
+                                 fmmt_format format, const std::vector<int64_t>& ranks, const std::vector<const void*>& full,
+                                 fmmt_op** op) {
+  return bcast_and_create(ctx, n1, n2, n3, ndir, b, c, format, ranks, full, op);
+}
+
+static fmmt_status compress_impl(fmmt_ctx* ctx, const fmmt_c128* T, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
+                                 int64_t dir_begin, int64_t dir_count, fmmt_format format, double tol, fmmt_op** op,
+                                 bool* sent) {
   if (!ctx || !op) return FMMT_E_ARG;
   *op = nullptr;
-  if (!T) return set_err(ctx, FMMT_E_ARG, "null T");
+  const bool is4d = format == FMMT_TUCKER4D || format == FMMT_HTUCKER4D || format == FMMT_TT4D;
+  // sharded 4D setup: rank 0 compresses the whole T_4D and broadcasts the shared factors and
+  // the direction factor; every rank keeps the rows of its own directions.  Other ranks pass T = NULL.
+  const bool bcast = is4d && ctx->world > 1;
+  const bool receiver = bcast && ctx->rank != 0;
+  if (!T && !receiver) return set_err(ctx, FMMT_E_ARG, "null T");
   if (!(tol > 0 && tol < 1)) return set_err(ctx, FMMT_E_ARG, "tol must be in (0,1)");
   if (format < FMMT_DENSE || format > FMMT_TT4D) return set_err(ctx, FMMT_E_ARG, "bad format");
   if (n1 < 2 || n2 < 2 || n3 < 2 || ndir < 1 || dir_begin < 0 || dir_count < 1 || dir_begin + dir_count > ndir)
     return set_err(ctx, FMMT_E_SHAPE, "bad compress shape");
+  const int64_t shard_begin = dir_begin, shard_count = dir_count;
   cudaSetDevice(ctx->device);
+  if (receiver) return compress_receive(ctx, n1, n2, n3, ndir, dir_begin, dir_count, format, op);
   Setup S;
   S.ctx = ctx;
   SETUP_TRY(handles(ctx, &S.blas, &S.sol));
   const int64_t n = n1 * n2 * n3;
+  if (bcast) {   // the root keeps every direction row until the broadcast; sliced below
+    dir_begin = 0;
+    dir_count = ndir;
+  }
   // T may be host or device memory
   cudaPointerAttributes pa;
   const double2* Td = nullptr;
@@ -835,8 +924,30 @@ extern "C" fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t 
   }
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   static const int narr_of[] = {1, 4, 5, 7, 3, 4};
+  if (bcast) {
+    *sent = true;
+    return compress_send(ctx, n1, n2, n3, ndir, shard_begin, shard_count, format, ranks, arrs, op);
+  }
   return fmmt_internal::create_op(ctx, format, n1, n2, n3, dir_count, ranks.empty() ? nullptr : ranks.data(), arrs.data(),
-                                  narr_of[format], op);
+                                  narr_of[format], op, true);
+}
+
+extern "C" fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
+                                     int64_t dir_begin, int64_t dir_count, fmmt_format format, double tol, fmmt_op** op) {
+  bool sent = false;
+  fmmt_status st = compress_impl(ctx, T, n1, n2, n3, ndir, dir_begin, dir_count, format, tol, op, &sent);
+  const bool is4d = format == FMMT_TUCKER4D || format == FMMT_HTUCKER4D || format == FMMT_TT4D;
+  if (st != FMMT_OK && !sent && ctx && ctx->world > 1 && ctx->rank == 0 && is4d && ctx->nccl_comm) {
+    // the root failed before its broadcast: send an all-zero rank header so the other ranks return
+    // FMMT_E_STATE instead of waiting forever (the root keeps its own error message)
+    std::string err = ctx->err;
+    DBuf hdr;
+    if (dalloc(ctx, hdr, 6 * 8) == FMMT_OK && cudaMemsetAsync(hdr.p, 0, 48, ctx->stream) == cudaSuccess &&
+        ncclBroadcast(hdr.p, hdr.p, 6, ncclInt64, 0, (ncclComm_t)ctx->nccl_comm, ctx->stream) == ncclSuccess)
+      cudaStreamSynchronize(ctx->stream);
+    ctx->err = err;
+  }
+  return st;
 }
 
 // ============================================================== FP64 derived operands (setup)

@@ -462,13 +462,21 @@ __global__ void k_dirsum_partial(const float2* __restrict__ sig, const float* __
   partial[(int64_t)s * K + v] = acc;
 }
 
+// One warp per output element: lane s adds partials s, s + 32, ... (nsplit <= 64), then a
+// shuffle reduction (the split count, not K, sets the parallelism when K is small).
 __global__ void k_dirsum_final(const float2* __restrict__ partial, float2* __restrict__ out,
                                int64_t K, int nsplit) {
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (v >= K) return;
   float2 acc = make_float2(0.f, 0.f);
-  for (int s = 0; s < nsplit; ++s) acc = cadd(acc, partial[(int64_t)s * K + v]);
-  out[v] = acc;
+  for (int s = lane; s < nsplit; s += 32) acc = cadd(acc, partial[(int64_t)s * K + v]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if (lane == 0) out[v] = acc;
 }
 
 }  // namespace fmmt

@@ -41,7 +41,7 @@ class fmmt_op_info_t(C.Structure):
     _fields_ = [("format", C.c_int32), ("n1", i64), ("n2", i64), ("n3", i64), ("ndir", i64),
                 ("rank_max", i64 * 6), ("rank_mean", C.c_double * 6), ("nranks", i64),
                 ("compressed_bytes", i64), ("original_bytes", i64), ("workspace_bytes", i64),
-                ("batch", i64), ("restore_cmac", C.c_double)]
+                ("batch", i64), ("restore_cmac", C.c_double), ("translatable", i64)]
 
 
 def _sig(name, res, *args):
@@ -73,6 +73,7 @@ fmmt_op_import = _sig("fmmt_op_import", C.c_int, vp, C.c_int, i64, i64, i64, i64
 fmmt_op_destroy = _sig("fmmt_op_destroy", None, vp)
 fmmt_op_info = _sig("fmmt_op_info", C.c_int, vp, C.POINTER(fmmt_op_info_t))
 fmmt_op_ranks = _sig("fmmt_op_ranks", C.c_int, vp, i64p, i64, i64p)
+fmmt_op_export = _sig("fmmt_op_export", C.c_int, vp, i64, vp, i64, i64p)
 fmmt_op_set_batch = _sig("fmmt_op_set_batch", C.c_int, vp, i64)
 fmmt_translate = _sig("fmmt_translate", C.c_int, vp, vp, vp, i64, i64, i64, i64)
 fmmt_translate_sum = _sig("fmmt_translate_sum", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, i64)
@@ -90,7 +91,7 @@ EXPORTED = [
     "fmmt_version", "fmmt_init", "fmmt_init_sharded", "fmmt_nccl_unique_id", "fmmt_destroy", "fmmt_sync",
     "fmmt_last_error", "fmmt_shard_range", "fmmt_set_profiling", "fmmt_prof_reset", "fmmt_prof_read",
     "fmmt_launch_count", "fmmt_multipole_count", "fmmt_direction_grid", "fmmt_build_operator", "fmmt_compress",
-    "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_set_batch", "fmmt_translate",
+    "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_export", "fmmt_op_set_batch", "fmmt_translate",
     "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
     "fmmt_translate_multi", "fmmt_translate_sum_multi", "fmmt_build_operator_lossy",
     "fmmt_aggregate", "fmmt_disaggregate", "fmmt_far_matvec",
@@ -195,10 +196,10 @@ class Context:
         return {names[i].decode(): (ms[i], la[i]) for i in range(min(64, cnt.value))}
 
     def set_gemm_impl(self, impl: str):
-        _check(fmmt_set_gemm_impl(self.h, {"ffma": 0, "tc": 1, "tc1": 2}[impl]), self.h, "fmmt_set_gemm_impl")
+        _check(fmmt_set_gemm_impl(self.h, {"ffma": 0, "tc": 1}[impl]), self.h, "fmmt_set_gemm_impl")
 
     def test_cgemm(self, impl: str, m, n, k, A, lda, B, ldb, Cout, ldc, transA=0, transB=0):
-        _check(fmmt_test_cgemm(self.h, {"ffma": 0, "tc": 1, "tc1": 2}[impl], m, n, k, transA, transB, _ptr(A), lda, _ptr(B), ldb,
+        _check(fmmt_test_cgemm(self.h, {"ffma": 0, "tc": 1}[impl], m, n, k, transA, transB, _ptr(A), lda, _ptr(B), ldb,
                                _ptr(Cout), ldc), self.h, "fmmt_test_cgemm")
 
     def build_operator(self, Nx, Ny, Nz, edge, k, L, khat: np.ndarray, out):
@@ -212,6 +213,8 @@ class Context:
                                          len(khat), _ptr(out)), self.h, "fmmt_build_operator_lossy")
 
     def compress(self, T, n, ndir, fmt, tol, dir_begin=0, dir_count=None) -> "Op":
+        """T: complex128 [ndir][n3][n2][n1] (host or device).  Sharded 4D formats (world > 1): rank 0
+        passes the whole T_4D, the other ranks pass T=None (the factors are broadcast)."""
         fmt = FORMATS[fmt] if isinstance(fmt, str) else fmt
         dir_count = ndir - dir_begin if dir_count is None else dir_count
         h = vp()
@@ -266,7 +269,20 @@ class Op:
         return dict(format=FORMAT_NAMES[i.format], n=(i.n1, i.n2, i.n3), ndir=i.ndir,
                     rank_max=list(i.rank_max[:nr]), rank_mean=list(i.rank_mean[:nr]),
                     compressed_bytes=i.compressed_bytes, original_bytes=i.original_bytes,
-                    workspace_bytes=i.workspace_bytes, batch=i.batch, restore_cmac=i.restore_cmac)
+                    workspace_bytes=i.workspace_bytes, batch=i.batch, restore_cmac=i.restore_cmac,
+                    translatable=bool(i.translatable))
+
+    def export(self) -> list:
+        """The op's complex64 factor arrays, in fmmt_op_import order (flat, library layout)."""
+        fmt = self.info()["format"]
+        out = []
+        for idx in range(NARRAYS[FORMATS[fmt]]):
+            cnt = C.c_int64()
+            _check(fmmt_op_export(self.h, idx, None, 0, C.byref(cnt)), self.ctx.h, "fmmt_op_export")
+            a = np.zeros(max(1, cnt.value), dtype=np.complex64)
+            _check(fmmt_op_export(self.h, idx, a.ctypes.data, len(a), C.byref(cnt)), self.ctx.h, "fmmt_op_export")
+            out.append(a[:cnt.value])
+        return out
 
     def ranks(self) -> np.ndarray:
         cnt = C.c_int64()

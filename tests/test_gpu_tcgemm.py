@@ -40,7 +40,7 @@ SHAPES = [(128, 64, 16), (300, 70, 45), (1, 1, 1), (129, 17, 17), (1024, 32, 27)
           (961, 130, 351), (32, 729, 27), (257, 33, 8), (1024, 64, 1201)]
 
 
-@pytest.mark.parametrize("impl", ["tc", "tc1", "ffma"])
+@pytest.mark.parametrize("impl", ["tc", "ffma"])
 @pytest.mark.parametrize("transA", [0, 1])
 @pytest.mark.parametrize("transB", [0, 1])
 @pytest.mark.parametrize("m,n,k", SHAPES)
