@@ -273,6 +273,11 @@ struct fmmt_op {
   };
   std::vector<GraphEntry> graphs;
   bool translatable = true;                    // false: storage-only op (compress beyond the translate shapes)
+  // fp16-split operand scales: device max(|Re|, |Im|) slots.  [0, 7) factor arrays, 7 TT-4D T1, 8 H-Tucker E
+  // (set once per op); from SLOT_DYN on, 4 per batch for the intermediates its launches produce (reset to 0
+  // at the start of every matvec; the producing GEMM folds its max |C| in, the consumer derives its scale)
+  float* d_slots = nullptr;
+  int64_t nslots_dyn = 0;
   // host staging for translate_sum_host
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
@@ -349,6 +354,12 @@ void fmmt_op_destroy(fmmt_op* op) {
   delete op;
 }
 
+constexpr int SLOT_T1 = 7, SLOT_E = 8, SLOT_DYN = 16, SLOTS_PER_BATCH = 4;
+static const float* sslot(const fmmt_op* op, int i) { return op->d_slots + i; }
+static float* dslot(const fmmt_op* op, int batch, int stage) {
+  return op->d_slots + SLOT_DYN + (int64_t)batch * SLOTS_PER_BATCH + stage;
+}
+
 // per-direction workspace bytes for batch sizing: every buffer sized by the batch (PB directions)
 static int64_t per_dir_ws(const fmmt_op* op) {
   const int64_t n12 = op->n1 * op->n2;
@@ -373,6 +384,23 @@ static int64_t per_dir_ws(const fmmt_op* op) {
 
 static fmmt_status cmalloc(fmmt_op* op, float2** p, int64_t elems) {
   return dev_alloc(op, p, std::max<int64_t>(elems, 1) * 8, MEM_WORKSPACE, "workspace");
+}
+
+// Fold max(|Re|, |Im|) of a flat complex64 array into a scale slot (asynchronous).
+static fmmt_status absmax_ctx(fmmt_ctx* ctx, const float2* x, int64_t n, float* slot) {
+  if (n <= 0) return FMMT_OK;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
+  fmmt::k_absmax<<<grid, 256, 0, ctx->stream>>>(x, n, slot);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+static fmmt_status absmax(fmmt_op* op, const float2* x, int64_t n, float* slot) { return absmax_ctx(op->ctx, x, n, slot); }
+
+// Reset the per-batch (dynamic) scale slots: at the start of every matvec / restore (a memset node when captured).
+static fmmt_status reset_dyn_slots(fmmt_op* op) {
+  if (!op->d_slots || op->nslots_dyn <= 0) return FMMT_OK;
+  FMMT_CUDA(op->ctx, cudaMemsetAsync(op->d_slots + SLOT_DYN, 0, op->nslots_dyn * 4, op->ctx->stream));
+  return FMMT_OK;
 }
 
 static void add_gemm(fmmt_op* op, Batch& b, const std::vector<GemmDesc>& ds, const char* name) {
@@ -491,18 +519,19 @@ static int tc_bn_for(int64_t n) { return n >= 32 ? 32 : 16; }   // as add_gemm p
 static int64_t packb_floats(const GemmDesc& d) {
   const int bn = tc_bn_for(d.n);
   const int64_t nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (d.n + bn - 1) / bn;
-  return (int64_t)d.batch * tiles_n * nkc * (64 * bn);   // BP_FLOATS = 64 BN
+  return (int64_t)d.batch * tiles_n * nkc * (64 * bn * fmmt::TC_ESZ / 4);   // BP_FLOATS = 64 BN (tf32) / 32 BN (f16)
 }
 
 static fmmt_status launch_pack_b(fmmt_ctx* ctx, const GemmDesc& d, float* out) {
+  // (d.bmax: the scale slot of B, set by the plan)
   const int bn = tc_bn_for(d.n);
   const int64_t items = packb_floats(d) / (64 * bn) * bn * (fmmt::TC_BK / 2);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16));
   ProfScope ps(ctx, "pack_b");
   if (bn == 32)
-    fmmt::k_tc_pack_b<32><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out);
+    fmmt::k_tc_pack_b<32><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out, d.bmax);
   else
-    fmmt::k_tc_pack_b<16><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out);
+    fmmt::k_tc_pack_b<16><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out, d.bmax);
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;
 }
@@ -547,7 +576,7 @@ static fmmt_status with_packed_static(fmmt_op* op, GemmDesc& d) {
 
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
-static fmmt_status tucker_chain(fmmt_op* op, Batch& b) {
+static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
   // Fig. 3(a) in the "tall" orientation so every GEMM has >= n1*r rows:
   //   mode 1:  H_q[(b + r2 c) + r2 r3 i] = sum_a core_q[a + r1 (b + r2 c)] U1[i + n1 a]
   //   mode 2:  G_q[i + n1 j + n12 c]     = sum_b H_q[b + r2 c + r2 r3 i] U2[j + n2 b]
@@ -564,18 +593,34 @@ static fmmt_status tucker_chain(fmmt_op* op, Batch& b) {
       float2* Hq = op->H + q * n1 * op->r2max * op->r3max;
       float2* Gq = op->Gw + q * n12 * op->rGmax;
       GemmDesc d1 = gdx(core, U1, Hq, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3);
+      d1.amax = sslot(op, 0);
+      d1.bmax = sslot(op, 1);
+      d1.cmax = dslot(op, bi, 0);
       if (fmmt_status st = with_packed_static(op, d1)) return st;
       sa.push_back(d1);
-      sb.push_back(gdx(Hq, U2, Gq, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1));
+      GemmDesc d2 = gdx(Hq, U2, Gq, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1);
+      d2.amax = dslot(op, bi, 0);
+      d2.bmax = sslot(op, 2);
+      d2.cmax = dslot(op, bi, 1);
+      sb.push_back(d2);
     }
   } else {
     const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
     const float2* U1 = op->arr[op->format == FMMT_TUCKER4D ? 1 : 0];
     const float2* U2 = op->arr[op->format == FMMT_TUCKER4D ? 2 : 1];
-    sa.push_back(gdx(op->Cw, U1, op->H, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3, b.nq,
-                     r1 * r2 * r3, 0, n1 * r2 * r3));
-    sb.push_back(gdx(op->H, U2, op->Gw, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1, b.nq,
-                     n1 * r2 * r3, 0, n12 * r3));
+    // (Tucker-4D: the slice GEMM wrote C_q with max into stage 0)
+    GemmDesc d1 = gdx(op->Cw, U1, op->H, r2 * r3, n1, r1, r1, 0, NODIV, 1, n1, 1, 1, 0, NODIV, r2 * r3, b.nq,
+                      r1 * r2 * r3, 0, n1 * r2 * r3);
+    d1.amax = dslot(op, bi, 0);
+    d1.bmax = sslot(op, 1);
+    d1.cmax = dslot(op, bi, 1);
+    sa.push_back(d1);
+    GemmDesc d2 = gdx(op->H, U2, op->Gw, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1, b.nq,
+                      n1 * r2 * r3, 0, n12 * r3);
+    d2.amax = dslot(op, bi, 1);
+    d2.bmax = sslot(op, 2);
+    d2.cmax = dslot(op, bi, 2);
+    sb.push_back(d2);
   }
   add_gemm(op, b, sa, "restore_mode1");
   add_gemm(op, b, sb, "restore_mode2");
@@ -638,23 +683,38 @@ static fmmt_status build_plans(fmmt_op* op) {
       if ((st = cmalloc(op, &op->Vw, PB * rk(op, 0, 1) * n3))) return st;
       break;
   }
+  const int64_t nbatches = (op->ndir + PB - 1) / PB;
+  if (op->nslots_dyn < nbatches * SLOTS_PER_BATCH) {   // scale slots (see fmmt_op::d_slots)
+    float* ns = nullptr;
+    if ((st = dev_alloc(op, &ns, (SLOT_DYN + nbatches * SLOTS_PER_BATCH) * 4, MEM_WORKSPACE, "scale slots"))) return st;
+    FMMT_CUDA(op->ctx, cudaMemsetAsync(ns, 0, (SLOT_DYN + nbatches * SLOTS_PER_BATCH) * 4, op->ctx->stream));
+    if (op->d_slots)
+      FMMT_CUDA(op->ctx, cudaMemcpyAsync(ns, op->d_slots, SLOT_DYN * 4, cudaMemcpyDeviceToDevice, op->ctx->stream));
+    dev_free(op, op->d_slots);
+    op->d_slots = ns;
+    op->nslots_dyn = nbatches * SLOTS_PER_BATCH;
+  }
   for (int64_t q0 = 0; q0 < op->ndir; q0 += PB) {
     Batch b;
+    const int bi = (int)(q0 / PB);
     b.q0 = (int)q0;
     b.nq = (int)std::min<int64_t>(PB, op->ndir - q0);
     switch (op->format) {
       case FMMT_DENSE: break;
       case FMMT_TUCKER3D:
-        if ((st = tucker_chain(op, b))) return st;
+        if ((st = tucker_chain(op, b, bi))) return st;
         break;
       case FMMT_TUCKER4D: {
         const int64_t r1 = rk(op, 0, 0), r2 = rk(op, 0, 1), r3 = rk(op, 0, 2), r4 = rk(op, 0, 3);
         // a3 (Fig. 3(b)): C_q = C(r1 r2 r3 x r4) . U4[p,:]^T
         GemmDesc ds = gd(op->arr[0], op->arr[4] + b.q0, op->Cw, r1 * r2 * r3, b.nq, r4, 1, r1 * r2 * r3, op->ndir, r1 * r2 * r3);
+        ds.amax = sslot(op, 0);
+        ds.bmax = sslot(op, 4);
+        ds.cmax = dslot(op, bi, 0);
         if ((st = with_packed_a(op, 0, ds))) return st;
         if ((st = with_packed_b_static(op, ds))) return st;
         add_gemm(op, b, {ds}, "slice_tucker4d");
-        if ((st = tucker_chain(op, b))) return st;
+        if ((st = tucker_chain(op, b, bi))) return st;
         break;
       }
       case FMMT_HTUCKER4D: {
@@ -666,10 +726,16 @@ static fmmt_status build_plans(fmmt_op* op) {
         const int64_t nq = b.nq;
         const float2 *U4 = op->arr[3], *C34 = op->arr[5];
         GemmDesc dm = gdx(C34, U4 + b.q0, op->Mw, r3 * r34, nq, r4, 1, r3 * r4, r3, r3, op->ndir, 1, 1, r3 * nq, r3, r3);
+        dm.amax = sslot(op, 5);
+        dm.bmax = sslot(op, 3);
+        dm.cmax = dslot(op, bi, 0);
         if ((st = with_packed_a(op, 5, dm))) return st;
         if ((st = with_packed_b_static(op, dm))) return st;
         add_gemm(op, b, {dm}, "slice_htucker_M");
         GemmDesc dg = gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12);
+        dg.amax = sslot(op, SLOT_E);
+        dg.bmax = dslot(op, bi, 0);
+        dg.cmax = dslot(op, bi, 1);
         dg.Ap = op->E_pk;
         dg.a_nkc = (int)((r34 + fmmt::TC_BK - 1) / fmmt::TC_BK);
         float* mpk = nullptr;
@@ -698,6 +764,9 @@ static fmmt_status build_plans(fmmt_op* op) {
           const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1);
           GemmDesc dh = gdx(op->arr[1] + op->off[1][p], op->arr[0] + op->off[0][p], op->Gw + q * n12 * op->rGmax,
                             n2 * r2, n1, r1, r1, 0, NODIV, 1, n1, 1, n1, n12, n2, 1);
+          dh.amax = sslot(op, 1);
+          dh.bmax = sslot(op, 0);
+          dh.cmax = dslot(op, bi, 0);
           if ((st = with_packed_static(op, dh))) return st;
           ds.push_back(dh);
         }
@@ -708,6 +777,9 @@ static fmmt_status build_plans(fmmt_op* op) {
         const int64_t r2 = rk(op, 0, 1), r3 = rk(op, 0, 2);
         // a3 (Fig. 4(b) step 1, columns of T2 for the batch): V_q = C2(r2 n3 x r3) . U_last[p,:]^T
         GemmDesc dv = gd(op->arr[2], op->arr[3] + b.q0, op->Vw, r2 * n3, b.nq, r3, 1, r2 * n3, op->ndir, r2 * n3);
+        dv.amax = sslot(op, 2);
+        dv.bmax = sslot(op, 3);
+        dv.cmax = dslot(op, bi, 0);
         if ((st = with_packed_a(op, 2, dv))) return st;
         if ((st = with_packed_b_static(op, dv))) return st;
         add_gemm(op, b, {dv}, "slice_tt4d");
@@ -803,7 +875,7 @@ static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* ou
   return FMMT_OK;
 }
 
-static void fill_zargs(fmmt_op* op, ZArgs& a) {
+static void fill_zargs(fmmt_op* op, ZArgs& a, int bi) {
   const int64_t n12 = op->n1 * op->n2;
   memset(&a, 0, sizeof(a));
   a.n12 = n12;
@@ -812,21 +884,26 @@ static void fill_zargs(fmmt_op* op, ZArgs& a) {
     case FMMT_TUCKER3D:
       a.G = op->Gw; a.g_stride = n12 * op->rGmax;
       a.V = op->arr[3]; a.v_off = op->d_voff; a.v_sc = op->n3; a.v_sk = 1; a.rank_p = op->d_rank;
+      a.amax = dslot(op, bi, 1); a.bmax = sslot(op, 3);
       break;
     case FMMT_TUCKER4D:
       a.G = op->Gw; a.g_stride = n12 * rk(op, 0, 2);
       a.V = op->arr[3]; a.v_stride = 0; a.v_sc = op->n3; a.v_sk = 1; a.rank = (int)rk(op, 0, 2);
+      a.amax = dslot(op, bi, 2); a.bmax = sslot(op, 3);
       break;
     case FMMT_HTUCKER4D:
       a.G = op->Gw; a.g_stride = n12 * rk(op, 0, 2);
       a.V = op->arr[2]; a.v_stride = 0; a.v_sc = op->n3; a.v_sk = 1; a.rank = (int)rk(op, 0, 2);
+      a.amax = dslot(op, bi, 1); a.bmax = sslot(op, 2);
       break;
     case FMMT_TT3D:
+      a.amax = dslot(op, bi, 0); a.bmax = sslot(op, 2);
       a.G = op->Gw; a.g_stride = n12 * op->rGmax;
       a.V = op->arr[2]; a.v_off = op->d_voff; a.v_sc = op->n3; a.v_sk = 1; a.rank_p = op->d_rank;
       break;
     case FMMT_TT4D:
       a.G = op->tbar1; a.g_stride = 0; a.Gp = op->tbar1_pk;
+      a.amax = sslot(op, SLOT_T1); a.bmax = dslot(op, bi, 0);
       // T1 pre-split = 16 B per complex: block the z-stage tiles by direction when it exceeds ~1/4 of L2
       a.z_blocked = n12 * rk(op, 0, 1) * 16 > (32ll << 20) ? 1 : 0;
       a.V = op->Vw; a.v_stride = rk(op, 0, 1) * op->n3; a.v_sc = 1; a.v_sk = rk(op, 0, 1); a.rank = (int)rk(op, 0, 1);
@@ -850,7 +927,7 @@ static fmmt_status pack_v_bn(fmmt_op* op, ZArgs& a, int nq) {
     ProfScope ps(ctx, "pack_v");
     const int64_t items = need / Cfg::BP_FLOATS * BN * (fmmt::TC_BK / 2);
     const unsigned grid = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
-    fmmt::k_tc_pack_b<BN><<<grid, 256, 0, ctx->stream>>>(a.V, a.v_stride, a.v_sc, a.v_sk, k, n, nq, op->Vpk);
+    fmmt::k_tc_pack_b<BN><<<grid, 256, 0, ctx->stream>>>(a.V, a.v_stride, a.v_sc, a.v_sk, k, n, nq, op->Vpk, a.bmax);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
   a.Vp = op->Vpk;
@@ -903,7 +980,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 == 64) {
     // tensor-core z-stage for n3 = 64: two parity passes, even-pass partial in op->zscr
     ZArgs a;
-    fill_zargs(op, a);
+    fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
     a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
     a.ncomp = ncomp;
     a.p0 = p0;
@@ -924,7 +1001,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
       const unsigned g2 = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
       for (int h = 0; h < 2; ++h)
         fmmt::k_tc_pack_b<32><<<g2, 256, 0, ctx->stream>>>(a.V + (int64_t)h * a.v_sk, a.v_stride, a.v_sc, 2 * a.v_sk, k,
-                                                            32, nq, op->Vpk + (int64_t)h * nq * per_q);
+                                                            32, nq, op->Vpk + (int64_t)h * nq * per_q, a.bmax);
       FMMT_CUDA(ctx, cudaGetLastError());
       a.Vp = op->Vpk;
       a.vp_stride = per_q;
@@ -947,7 +1024,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   }
   if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
     ZArgs a;
-    fill_zargs(op, a);
+    fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
     a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
     a.ncomp = ncomp;
     a.p0 = p0;
@@ -973,7 +1050,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   ZKernel k = get_z((int)op->n3, mode);
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
   ZArgs a;
-  fill_zargs(op, a);
+  fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
   a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
   a.ncomp = ncomp;
   a.p0 = p0;
@@ -1020,7 +1097,7 @@ static fmmt_status ensure_vpk(fmmt_op* op) {
   const int BN = op->n3 <= 16 ? 16 : 32;
   const int64_t nkc = (rk(op, 0, 1) + fmmt::TC_BK - 1) / fmmt::TC_BK;
   const int64_t tiles_n = op->n3 == 64 ? 2 : (op->n3 + BN - 1) / BN;   // n3 = 64: one 32-column pack per parity pass
-  const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK);   // BP_FLOATS = 2 NR x 2 BK, NR = 2 BN
+  const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK * fmmt::TC_ESZ / 4);   // BP_FLOATS: 2 NR x 2 BK, NR = 2 BN
   if (op->vpk_floats >= need) return FMMT_OK;
   drop_graphs(op);
   dev_free(op, op->Vpk);
@@ -1053,6 +1130,7 @@ static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64*
   // z-stage (one restore of T_p serves all ncomp components); a6: one launch back.
   fmmt_status st;
   const int planes = (int)(op->ndir * ncomp * Nz);
+  if ((st = reset_dyn_slots(op))) return st;
   if ((st = launch_xy(op, true, in, op->W, planes, 1.f))) return st;
   for (const Batch& b : op->batches) {
     if ((st = run_batch_prep(op, b))) return st;
@@ -1298,7 +1376,17 @@ fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64
   GemmDesc d = gd(reinterpret_cast<const float2*>(A), reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(C),
                   m, n, k, transB, lda, ldb, ldc);
   if (transA) { d.a_s0 = lda; d.a_sk = 1; }
-  return run_one_gemm(ctx, d, impl, "test_cgemm");
+  // operand scales of the fp16 split over the referenced extents
+  float* sl = nullptr;
+  FMMT_CUDA(ctx, cudaMallocAsync((void**)&sl, 8, ctx->stream));
+  FMMT_CUDA(ctx, cudaMemsetAsync(sl, 0, 8, ctx->stream));
+  fmmt_status st = absmax_ctx(ctx, d.A, (m - 1) * d.a_s0 + (k - 1) * d.a_sk + 1, sl);
+  if (!st) st = absmax_ctx(ctx, d.B, (k - 1) * d.b_sk + (n - 1) * d.b_sn + 1, sl + 1);
+  d.amax = sl;
+  d.bmax = sl + 1;
+  if (!st) st = run_one_gemm(ctx, d, impl, "test_cgemm");
+  cudaFreeAsync(sl, ctx->stream);
+  return st;
 }
 
 fmmt_status fmmt_op_import(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2, int64_t n3, int64_t ndir,
@@ -1701,6 +1789,7 @@ fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
     return FMMT_OK;
   }
   if (fmmt_status st = ensure_vpk(op)) return st;
+  if (fmmt_status st = reset_dyn_slots(op)) return st;
   for (const Batch& b : op->batches) {
     if (p < b.q0 || p >= b.q0 + b.nq) continue;
     fmmt_status st = run_batch_prep(op, b);
@@ -1846,6 +1935,16 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     *out = op;
     return FMMT_OK;
   }
+  {  // fp16-split scale slots of the factor arrays (fmmt_op::d_slots)
+    fmmt_status st = dev_alloc(op, &op->d_slots, SLOT_DYN * 4, MEM_WORKSPACE, "scale slots");
+    if (!st && cudaMemsetAsync(op->d_slots, 0, SLOT_DYN * 4, ctx->stream) != cudaSuccess)
+      st = set_err(ctx, FMMT_E_CUDA, "scale slot reset failed");
+    for (size_t i = 0; !st && i < elems.size(); ++i) st = absmax(op, op->arr[i], elems[i], op->d_slots + i);
+    if (st) {
+      fmmt_op_destroy(op);
+      return st;
+    }
+  }
   if (format == FMMT_HTUCKER4D) {
     // Direction-independent part of Fig. 3(c), once per op, in FP64 (setup):
     //   E[i + n1 jj + n12 j] = sum_{a,b} U1[i,a] U2[jj,b] (C12 . C1234)[a + r1 b, j]
@@ -1856,12 +1955,14 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     }
     fmmt_status st = fmmt_internal::htucker_E_fp64(ctx, op->arr[0], op->arr[1], op->arr[4], op->arr[6], n1, n2, r1, r2,
                                                    r12, r34, op->E);
+    if (!st) st = absmax(op, op->E, n12 * r34, op->d_slots + SLOT_E);
     if (st) {
       fmmt_op_destroy(op);
       return st;
     }
-    if (ctx->pack_factors &&
-        (st = pack_a(op, gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0), &op->E_pk))) {
+    GemmDesc de = gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0);
+    de.amax = sslot(op, SLOT_E);
+    if (ctx->pack_factors && (st = pack_a(op, de, &op->E_pk))) {
       fmmt_op_destroy(op);
       return st;
     }
@@ -1879,15 +1980,15 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
       return ast;
     }
     fmmt_status tst = fmmt_internal::tt4d_T1_fp64(ctx, op->arr[0], op->arr[1], n1, r1, n2, r2, op->tbar1);
+    const int64_t n12 = n1 * n2;
+    if (!tst) tst = absmax(op, op->tbar1, n12 * r2, op->d_slots + SLOT_T1);
     if (tst) {
       fmmt_op_destroy(op);
       return tst;
     }
-    const int64_t n12 = n1 * n2;
-    fmmt_status pst = ctx->pack_factors
-                          ? pack_a(op, gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0),
-                                   &op->tbar1_pk)
-                          : FMMT_OK;
+    GemmDesc dt = gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0);
+    dt.amax = sslot(op, SLOT_T1);
+    fmmt_status pst = ctx->pack_factors ? pack_a(op, dt, &op->tbar1_pk) : FMMT_OK;
     if (pst) {
       fmmt_op_destroy(op);
       return pst;

@@ -319,6 +319,8 @@ struct ZArgs {
   const float* Vp;           // V pre-split for the tensor-core kernel (k_tc_pack_b), or nullptr
   int64_t vp_stride;         // floats per batch-local q
   int z_blocked;             // tensor-core z-stage: direction-blocked tile order (shared A larger than L2 share)
+  const float* amax;         // fp16-split scales: device max |G| (A) and max |V| (B); nullptr = unit scale
+  const float* bmax;
   // dense operator: T[p][k][ij]
   const float2* T;
   // restore output [k][ij]

@@ -39,6 +39,12 @@ struct GemmDesc {
   // tensor-core tile order: 0 = m-tiles fastest (B tile shared by consecutive CTAs), 1 = n-tiles fastest
   // (A tile shared; chosen when A is the larger operand, so it streams from DRAM once)
   int n_fast;
+  // fp16-split operand scales (kernels_tcgemm.cuh): device max(|Re|, |Im|) of A and B (the power-of-two
+  // scale is derived from it; packed operands were split with the same value), and the slot into which
+  // the kernel folds max |C| for the consumer of C; nullptr = none / unit scale
+  const float* amax;
+  const float* bmax;
+  float* cmax;
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {

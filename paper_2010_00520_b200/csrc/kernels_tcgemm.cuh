@@ -52,12 +52,27 @@ __device__ __forceinline__ void z_tile(int t, int tiles_m, int nq, bool shared_a
   q = qb * ZQB + r % qbs;
 }
 
+// Operand split (FMMT_TC_F16, build-time): 1 = fp16 hi + lo with a power-of-two operand scale
+// (kind::f16, 16 real K per MMA, twice the tf32 rate and half the operand bytes), 0 = TF32 hi + lo
+// (kind::tf32, 8 real K per MMA).  Both keep 11 + 11 significant bits per operand and FP32
+// accumulation; the products hi.hi + hi.lo + lo.hi (3 MMAs per useful MAC).
+#ifndef FMMT_TC_F16
+#define FMMT_TC_F16 1
+#endif
+#ifndef FMMT_TC_FC16
+#define FMMT_TC_FC16 4
+#endif
+constexpr bool TC_F16 = FMMT_TC_F16 != 0;
+constexpr int TC_ESZ = TC_F16 ? 2 : 4;   // bytes per split operand element in shared memory
+constexpr int TC_KSTEP = TC_F16 ? 16 : 8;   // real K per MMA instruction
 constexpr int TC_BM = 128;      // rows per tile (UMMA M)
-constexpr int TC_BK = 8;        // complex K per chunk (16 real = 2 UMMA K-steps)
+constexpr int TC_BK = 8;        // complex K per chunk (16 real: 1 f16 / 2 tf32 UMMA K-steps)
 constexpr int TC_NS = 4;        // operand ring stages: copies run 2 chunks ahead, MMAs of chunk k-1 overlap
                                 // the conversion of chunk k
-constexpr int TC_PACK_FLOATS = 2 * TC_BM * 2 * TC_BK;   // one packed A tile: hi + lo, 128 x 16 real
-constexpr int TC_FC = 2;        // chunks per TMEM flush group (4 K-steps per accumulator chain; 8 fails the 1e-6 restore bar)
+constexpr int TC_PACK_FLOATS = 2 * TC_BM * 2 * TC_BK * TC_ESZ / 4;   // one packed A chunk (hi + lo), in floats
+// chunks per TMEM flush group = MMAs chained into one accumulator before it is drained to FP32
+// registers: tf32 4 K-steps (8 failed the 1e-6 restore bar), f16 FMMT_TC_FC16 K-steps
+constexpr int TC_FC = TC_F16 ? FMMT_TC_FC16 : 2;
 
 template <int BN, int G = 1>
 struct TcGemmCfg {
@@ -65,13 +80,14 @@ struct TcGemmCfg {
   static constexpr int NR = 2 * BN;                 // real N of C (re, im interleaved)
   static constexpr int NRG = NR / G;                // real columns per thread group
   static constexpr int KR = 2 * TC_BK;              // real K per chunk
-  static constexpr int A_BYTES = TC_BM * KR * 4;    // one of hi / lo (16 KB)
+  static constexpr int A_BYTES = TC_BM * KR * TC_ESZ;   // one of hi / lo
   static constexpr int BP_ROWS = 2 * NR;            // B' = [B^_hi ; B^_lo]
-  static constexpr int BP_BYTES = BP_ROWS * KR * 4;
-  static constexpr int BP_FLOATS = BP_BYTES / 4;      // one pre-split B' chunk (k_tc_pack_b)
+  static constexpr int BP_BYTES = BP_ROWS * KR * TC_ESZ;
+  static constexpr int BP_FLOATS = BP_BYTES / 4;      // one pre-split B' chunk (k_tc_pack_b), in floats
   static constexpr int BITEMS = BN * (TC_BK / 2) / NT > 0 ? BN * (TC_BK / 2) / NT : 1;
   static constexpr int BRAW = BITEMS * NT * 16;     // raw B staging
-  static constexpr int STAGE = 2 * A_BYTES + BP_BYTES + BRAW;
+  static constexpr int ARAW = TC_F16 ? TC_BM * KR * 4 : 0;   // raw FP32 A staging (f16: split out of place)
+  static constexpr int STAGE = 2 * A_BYTES + BP_BYTES + ARAW + BRAW;
   static constexpr int SMEM = TC_NS * STAGE;
   // two accumulator slots (alternating K-chunks) x {hi.hi, hi.lo + lo.hi}
   static constexpr int TMEM_COLS = 4 * NR < 32 ? 32 : 4 * NR;
@@ -125,7 +141,8 @@ template <int BN, int G>
 __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __restrict__ A,
                                            const float2* __restrict__ B, int m0, int n0, uint8_t* tcsm,
                                            uint64_t* bar, uint32_t tmem,
-                                           float (&acc)[TcGemmCfg<BN, G>::NRG], TcCursor& cur) {
+                                           float (&acc)[TcGemmCfg<BN, G>::NRG], TcCursor& cur, float sA = 1.f,
+                                           float sB = 1.f) {
   using Cfg = TcGemmCfg<BN, G>;
   constexpr int BM = TC_BM, BK = TC_BK, NR = Cfg::NR, NRG = Cfg::NRG, NT = Cfg::NT;
   constexpr int BITEMS = Cfg::BITEMS;
@@ -143,8 +160,8 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     okrow[u] = m0 + r < d.m;
     arow[u] = okrow[u] ? a_row(d, m0 + r) : 0;
   }
-  constexpr uint32_t IDESC_BP = tc::idesc_tf32(BM, 2 * NR);   // A_hi x [B_hi ; B_lo]
-  constexpr uint32_t IDESC_B = tc::idesc_tf32(BM, NR);        // A_lo x B_hi
+  constexpr uint32_t IDESC_BP = TC_F16 ? tc::idesc_f16(BM, 2 * NR) : tc::idesc_tf32(BM, 2 * NR);   // A_hi x [B_hi ; B_lo]
+  constexpr uint32_t IDESC_B = TC_F16 ? tc::idesc_f16(BM, NR) : tc::idesc_tf32(BM, NR);            // A_lo x B_hi
 #pragma unroll
   for (int j = 0; j < NRG; ++j) acc[j] = 0.f;
   const uint32_t twarp = tmem + ((uint32_t)(wrow * 32) << 16);   // this warp's TMEM lanes
@@ -163,7 +180,12 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   const bool bpack = d.Bp != nullptr;   // B pre-split into B' chunks: one bulk copy per chunk
   const bool both_u = __shfl_sync(0xffffffffu, (int)(apack && bpack), 0);   // no per-thread operand work
   const float* apk = apack ? d.Ap + (int64_t)(m0 / BM) * d.a_nkc * TC_PACK_FLOATS : nullptr;
-  // copies of chunk c into stage c & 1: A straight into the canonical A_hi layout, B raw
+  // raw A lands in the canonical (TF32-layout) A_hi tile for the in-place tf32 split, in a staging
+  // area for the out-of-place fp16 split; raw B always in its staging area
+  constexpr int AR_OFF = TC_F16 ? 2 * Cfg::A_BYTES + Cfg::BP_BYTES : 0;
+  constexpr int BR_OFF = 2 * Cfg::A_BYTES + Cfg::BP_BYTES + Cfg::ARAW;
+  constexpr uint32_t LBO_AR = TC_BM * 16;   // raw FP32 A: K-adjacent 4-element groups
+  // copies of chunk c into stage c % NS
   auto issue = [&](int c) {
     const int k0 = c * BK;
     const int cs = (cur.c + c) % TC_NS;
@@ -182,7 +204,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
         const int kk = grp * (BK / G) + kq;
         const int gk = k0 + kk;
         const bool ok = okrow[0] && gk < d.k;
-        tc::cp_async8(st + row * 16 + (kk >> 1) * Cfg::LBO_A + (kk & 1) * 8,
+        tc::cp_async8(st + AR_OFF + row * 16 + (kk >> 1) * LBO_AR + (kk & 1) * 8,
                       ok ? (const void*)(A + arow[0] + gk * d.a_sk) : (const void*)A, ok);
       }
     } else {
@@ -197,12 +219,12 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
         const bool okr = (G == 1) ? okrow[uu] : (grp ? okrow[2 * uu + 1] : okrow[2 * uu]);
         const int64_t ar = (G == 1) ? arow[uu] : (grp ? arow[2 * uu + 1] : arow[2 * uu]);
         const bool ok0 = okr && gk < d.k, ok1 = okr && gk + 1 < d.k;
-        const uint32_t dst = st + r * 16 + kp * Cfg::LBO_A;
+        const uint32_t dst = st + AR_OFF + r * 16 + kp * LBO_AR;
         tc::cp_async8(dst, ok0 ? (const void*)(A + ar + gk) : (const void*)A, ok0);
         tc::cp_async8(dst + 8, ok1 ? (const void*)(A + ar + gk + 1) : (const void*)A, ok1);
       }
     }
-    const uint32_t rb = st + 2 * Cfg::A_BYTES + Cfg::BP_BYTES;
+    const uint32_t rb = st + BR_OFF;
 #pragma unroll
     for (int i = 0; i < BITEMS; ++i) {
       if (bpack) break;
@@ -223,7 +245,7 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
 
   // Barrier-free pipeline (no __syncthreads in the K loop).  Every thread converts exactly the
   // shared-memory segments its own cp.async copied, fences them for the async proxy and arrives
-  // on full[s]; thread 0 waits for the 128 arrivals, issues the chunk's MMAs and commits them to
+  // on full[s]; warp 0 waits for the 128 arrivals, issues the chunk's MMAs and commits them to
   // mma[s]; a stage is refilled once mma[s] completed; TMEM slots are handed back through tfree.
   //   bar[0, NS) mma commits   bar[NS, 2NS) packed-A bulk copies   bar[2NS, 3NS) full (128)
   //   bar[3NS, 3NS+2) tfree (128), one per TMEM slot
@@ -267,24 +289,34 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
     uint8_t* aHi = st;
     uint8_t* aLo = st + Cfg::A_BYTES;
     uint8_t* bP = st + 2 * Cfg::A_BYTES;
-    const uint8_t* bRaw = bP + Cfg::BP_BYTES;
-    // ---- round this thread's A segments in place to A_hi = rna_tf32(x), A_lo = rna_tf32(x - A_hi)
-    //      next to them.  Round-to-nearest on both parts keeps |x - hi - lo| and the dropped lo.lo
-    //      product at 2^-22 |x| (a truncated hi doubles both: measured restore errors up to 1.02e-6
-    //      against the 1e-6 bar).
+    const uint8_t* aRaw = st + AR_OFF;
+    const uint8_t* bRaw = st + BR_OFF;
+    // ---- split this thread's A segments: A_hi = rn(x), A_lo = rn(x - A_hi).  Round-to-nearest on
+    //      both parts keeps |x - hi - lo| and the dropped lo.lo product at 2^-22 |x| (a truncated hi
+    //      doubles both: measured restore errors up to 1.02e-6 against the 1e-6 bar).
     if (!apack) {
 #pragma unroll
       for (int u = 0; u < BK / 2; ++u) {
-        const uint32_t off = a_kcontig ? ((lane & 7) + 8 * (u + 4 * wrow)) * 16 + (lane >> 3) * Cfg::LBO_A
-                                       : row * 16 + u * Cfg::LBO_A;
-        const float4 a = *reinterpret_cast<const float4*>(aHi + off);
-        float4 hi, lo;
-        tc::split_tf32(a.x, hi.x, lo.x);
-        tc::split_tf32(a.y, hi.y, lo.y);
-        tc::split_tf32(a.z, hi.z, lo.z);
-        tc::split_tf32(a.w, hi.w, lo.w);
-        *reinterpret_cast<float4*>(aHi + off) = hi;
-        *reinterpret_cast<float4*>(aLo + off) = lo;
+        const int r = a_kcontig ? (lane & 7) + 8 * (u + 4 * wrow) : row;
+        const int kp = a_kcontig ? (lane >> 3) : u;      // complex pair = reals [4 kp, 4 kp + 4)
+        const float4 a = *reinterpret_cast<const float4*>(aRaw + r * 16 + kp * LBO_AR);
+        if constexpr (TC_F16) {
+          uint2 hi, lo;
+          tc::split_f16x2(a.x * sA, a.y * sA, hi.x, lo.x);
+          tc::split_f16x2(a.z * sA, a.w * sA, hi.y, lo.y);
+          const uint32_t off = r * 16 + (kp >> 1) * Cfg::LBO_A + (kp & 1) * 8;
+          *reinterpret_cast<uint2*>(aHi + off) = hi;
+          *reinterpret_cast<uint2*>(aLo + off) = lo;
+        } else {
+          const uint32_t off = r * 16 + kp * Cfg::LBO_A;
+          float4 hi, lo;
+          tc::split_tf32(a.x, hi.x, lo.x);
+          tc::split_tf32(a.y, hi.y, lo.y);
+          tc::split_tf32(a.z, hi.z, lo.z);
+          tc::split_tf32(a.w, hi.w, lo.w);
+          *reinterpret_cast<float4*>(aHi + off) = hi;
+          *reinterpret_cast<float4*>(aLo + off) = lo;
+        }
       }
     }
     // ---- B' rows: [0, NR) = B^_hi, [NR, 2NR) = B^_lo;  row 2j = [Re b, -Im b], row 2j+1 = [Im b, Re b]
@@ -296,18 +328,31 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       if (!b_kcontig) { j = idx % BN; kp = idx / BN; }
       else { kp = idx % (BK / 2); j = idx / (BK / 2); }
       const float4 bb = *reinterpret_cast<const float4*>(bRaw + (i * NT + tid) * 16);
-      const float4 r0 = make_float4(bb.x, -bb.y, bb.z, -bb.w);
-      const float4 r1 = make_float4(bb.y, bb.x, bb.w, bb.z);
-      const uint32_t off = (2 * j) * 16 + kp * Cfg::LBO_B;
-      float4 h0, l0, h1, l1;
-      tc::split_tf32(r0.x, h0.x, l0.x); tc::split_tf32(r0.y, h0.y, l0.y);
-      tc::split_tf32(r0.z, h0.z, l0.z); tc::split_tf32(r0.w, h0.w, l0.w);
-      tc::split_tf32(r1.x, h1.x, l1.x); tc::split_tf32(r1.y, h1.y, l1.y);
-      tc::split_tf32(r1.z, h1.z, l1.z); tc::split_tf32(r1.w, h1.w, l1.w);
-      *reinterpret_cast<float4*>(bP + off) = h0;
-      *reinterpret_cast<float4*>(bP + off + 16) = h1;
-      *reinterpret_cast<float4*>(bP + off + NR * 16) = l0;
-      *reinterpret_cast<float4*>(bP + off + NR * 16 + 16) = l1;
+      if constexpr (TC_F16) {
+        uint2 h0, l0, h1, l1;
+        tc::split_f16x2(bb.x * sB, -bb.y * sB, h0.x, l0.x);
+        tc::split_f16x2(bb.z * sB, -bb.w * sB, h0.y, l0.y);
+        tc::split_f16x2(bb.y * sB, bb.x * sB, h1.x, l1.x);
+        tc::split_f16x2(bb.w * sB, bb.z * sB, h1.y, l1.y);
+        const uint32_t off = (2 * j) * 16 + (kp >> 1) * Cfg::LBO_B + (kp & 1) * 8;
+        *reinterpret_cast<uint2*>(bP + off) = h0;
+        *reinterpret_cast<uint2*>(bP + off + 16) = h1;
+        *reinterpret_cast<uint2*>(bP + off + NR * 16) = l0;
+        *reinterpret_cast<uint2*>(bP + off + NR * 16 + 16) = l1;
+      } else {
+        const float4 r0 = make_float4(bb.x, -bb.y, bb.z, -bb.w);
+        const float4 r1 = make_float4(bb.y, bb.x, bb.w, bb.z);
+        const uint32_t off = (2 * j) * 16 + kp * Cfg::LBO_B;
+        float4 h0, l0, h1, l1;
+        tc::split_tf32(r0.x, h0.x, l0.x); tc::split_tf32(r0.y, h0.y, l0.y);
+        tc::split_tf32(r0.z, h0.z, l0.z); tc::split_tf32(r0.w, h0.w, l0.w);
+        tc::split_tf32(r1.x, h1.x, l1.x); tc::split_tf32(r1.y, h1.y, l1.y);
+        tc::split_tf32(r1.z, h1.z, l1.z); tc::split_tf32(r1.w, h1.w, l1.w);
+        *reinterpret_cast<float4*>(bP + off) = h0;
+        *reinterpret_cast<float4*>(bP + off + 16) = h1;
+        *reinterpret_cast<float4*>(bP + off + NR * 16) = l0;
+        *reinterpret_cast<float4*>(bP + off + NR * 16 + 16) = l1;
+      }
     }
     if (!both_u) tc::fence_async_smem();              // this thread's converted operands -> async proxy
     // every thread arrives, also with two pre-split operands (nothing converted): the full[] barrier
@@ -327,10 +372,15 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
       const uint64_t so = (uint64_t)((su * Cfg::STAGE) >> 4);   // descriptor start-address units
       const uint32_t tm = tmem_u + (g & 1) * 2 * NR, tx = tm + NR;
 #pragma unroll
-      for (int ks = 0; ks < Cfg::KR / 8; ++ks) {
+      for (int ks = 0; ks < Cfg::KR / TC_KSTEP; ++ks) {   // one K-step = two K-adjacent core matrices
         const uint64_t oa = so + ((ks * 2 * Cfg::LBO_A) >> 4), ob = so + ((ks * 2 * Cfg::LBO_B) >> 4);
-        tc::mma_tf32_el(tm, dAh + oa, dBp + ob, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
-        tc::mma_tf32_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);                       // += lo.hi (rows [0, NR))
+        if constexpr (TC_F16) {
+          tc::mma_f16_el(tm, dAh + oa, dBp + ob, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
+          tc::mma_f16_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);                       // += lo.hi (rows [0, NR))
+        } else {
+          tc::mma_tf32_el(tm, dAh + oa, dBp + ob, IDESC_BP, !(fresh && ks == 0));   // [hi.hi | hi.lo]
+          tc::mma_tf32_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);                       // += lo.hi (rows [0, NR))
+        }
       }
       tc::mma_commit_el(bar_u + su * 8);              // -> mmab[su]
     }
@@ -349,6 +399,11 @@ __device__ __forceinline__ void tc_mainloop(const GemmDesc& d, const float2* __r
   }
   cur.c += nk;
   cur.g += flushed;
+  if constexpr (TC_F16) {                            // undo the operand scales (exact: powers of two)
+    const float inv = 1.f / (sA * sB);
+#pragma unroll
+    for (int j = 0; j < NRG; ++j) acc[j] *= inv;
+  }
 }
 
 // TMEM allocation + stage barriers (all threads call; warp 0 allocates).
@@ -405,17 +460,24 @@ __global__ void __launch_bounds__(128 * G) k_tc_cgemm(const GemmDesc* __restrict
     const float2* __restrict__ B = d.B + (int64_t)sub * d.sB;
     float2* __restrict__ C = d.C + (int64_t)sub * d.sC;
     float acc[NRG];
-    tc_mainloop<BN, G>(d, A, B, m0, n0, tcsm, bar, tmem, acc, cur);
+    const float sA = (TC_F16 && d.amax) ? tc::f16_scale(*d.amax) : 1.f;
+    const float sB = (TC_F16 && d.bmax) ? tc::f16_scale(*d.bmax) : 1.f;
+    tc_mainloop<BN, G>(d, A, B, m0, n0, tcsm, bar, tmem, acc, cur, sA, sB);
     const int gm = m0 + (threadIdx.x & 127);
     const int nb = n0 + (threadIdx.x >> 7) * (BN / G);
+    float cm = 0.f;
     if (gm < d.m) {
       const int64_t crow = c_row(d, gm);
 #pragma unroll
       for (int j = 0; j < BN / G; ++j) {
         const int gn = nb + j;
-        if (gn < d.n) C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+        if (gn < d.n) {
+          C[crow + d.c_sn * (int64_t)gn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          cm = fmaxf(cm, fmaxf(fabsf(acc[2 * j]), fabsf(acc[2 * j + 1])));
+        }
       }
     }
+    if (d.cmax) tc::warp_absmax_to(cm, d.cmax);   // operand scale of the consumer of C
   }
   tc_teardown<Cfg::TMEM_COLS>(tmem);
 }
@@ -475,7 +537,11 @@ __global__ void __launch_bounds__(128 * G, 1) k_tc_conv_z(ZArgs a, int nq) {
     const bool valid = ij < a.n12;
 
     float acc[Cfg::NRG];
-    tc_mainloop<BN, G>(d, A, B, m0, 0, tcsm, bar, tmem, acc, cur);
+    const float sA = (TC_F16 && a.amax) ? tc::f16_scale(*a.amax) : 1.f;
+    const float sB = (TC_F16 && a.bmax) ? tc::f16_scale(*a.bmax) : 1.f;
+    d.amax = d.bmax = nullptr;
+    d.cmax = nullptr;
+    tc_mainloop<BN, G>(d, A, B, m0, 0, tcsm, bar, tmem, acc, cur, sA, sB);
 
     if constexpr (MODE == Z_RESTORE) {
       if (valid) {
@@ -553,10 +619,14 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
   const bool valid = ij < a.n12;
 
   float acc[2 * BN];
+  const float sA = (TC_F16 && a.amax) ? tc::f16_scale(*a.amax) : 1.f;
+  const float sB = (TC_F16 && a.bmax) ? tc::f16_scale(*a.bmax) : 1.f;
+  d.amax = d.bmax = nullptr;
+  d.cmax = nullptr;
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     d.Bp = a.Vp ? a.Vp + ((int64_t)h * nq + q) * a.vp_stride : nullptr;   // pre-split V_q columns 2j + h
-    tc_mainloop<BN, 1>(d, A, B, m0, h * H, tcsm, bar, tmem, acc, cur);   // T_p[ij, 2m + h]
+    tc_mainloop<BN, 1>(d, A, B, m0, h * H, tcsm, bar, tmem, acc, cur, sA, sB);   // T_p[ij, 2m + h]
     if constexpr (MODE == Z_RESTORE) {
       if (valid) {
 #pragma unroll
@@ -599,15 +669,16 @@ __global__ void __launch_bounds__(128, 1) k_tc_conv_z64(ZArgs a, float2* __restr
 
 // ---------------------------------------------------------------- k_tc_pack_a
 // Pre-split a (static) A operand into the tensor-core kernel's operand layout:
-// per (128-row tile, 16-complex K-chunk) one contiguous block of TC_PACK_FLOATS
-// floats = A_hi then A_lo (rna TF32 split), each in the canonical K-major UMMA
-// layout, zero-padded outside m x k.  The GEMM then streams A with one 32 KB
-// bulk async copy per chunk and no per-element work.  One thread per
-// (row, complex pair).
+// per (128-row tile, 8-complex K-chunk) one contiguous block of TC_PACK_FLOATS
+// floats = A_hi then A_lo (round-to-nearest split; fp16 after the power-of-two
+// scale of *d.amax, or TF32), each in the canonical K-major UMMA layout, zero-padded
+// outside m x k.  The GEMM then streams A with one bulk async copy per chunk and no
+// per-element work.  One thread per (row, complex pair).
 __global__ void k_tc_pack_a(GemmDesc d, float* __restrict__ out) {
   const int nkc = (d.k + TC_BK - 1) / TC_BK;
   const int64_t tiles_m = (d.m + TC_BM - 1) / TC_BM;
   const int64_t total = tiles_m * TC_BM * nkc * (TC_BK / 2);
+  const float s = (TC_F16 && d.amax) ? tc::f16_scale(*d.amax) : 1.f;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e % TC_BM);                       // row in tile (fastest: coalesced writes)
     int64_t t = e / TC_BM;
@@ -623,15 +694,24 @@ __global__ void k_tc_pack_a(GemmDesc d, float* __restrict__ out) {
       if (gk < d.k) a0 = d.A[row + (int64_t)gk * d.a_sk];
       if (gk + 1 < d.k) a1 = d.A[row + (int64_t)(gk + 1) * d.a_sk];
     }
-    float4 hi, lo;
-    tc::split_tf32(a0.x, hi.x, lo.x);
-    tc::split_tf32(a0.y, hi.y, lo.y);
-    tc::split_tf32(a1.x, hi.z, lo.z);
-    tc::split_tf32(a1.y, hi.w, lo.w);
-    float* tile = out + (tm * nkc + kc) * TC_PACK_FLOATS;
-    const int off = r * 4 + kp * (TC_BM * 4);             // floats: row r -> 16 B, K core matrix -> TC_BM*16 B
-    *reinterpret_cast<float4*>(tile + off) = hi;
-    *reinterpret_cast<float4*>(tile + TC_PACK_FLOATS / 2 + off) = lo;
+    uint8_t* tile = reinterpret_cast<uint8_t*>(out + (tm * nkc + kc) * TC_PACK_FLOATS);
+    if constexpr (TC_F16) {
+      uint2 hi, lo;
+      tc::split_f16x2(a0.x * s, a0.y * s, hi.x, lo.x);
+      tc::split_f16x2(a1.x * s, a1.y * s, hi.y, lo.y);
+      const int off = r * 16 + (kp >> 1) * (TC_BM * 16) + (kp & 1) * 8;   // bytes (fp16 core matrices)
+      *reinterpret_cast<uint2*>(tile + off) = hi;
+      *reinterpret_cast<uint2*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
+    } else {
+      float4 hi, lo;
+      tc::split_tf32(a0.x, hi.x, lo.x);
+      tc::split_tf32(a0.y, hi.y, lo.y);
+      tc::split_tf32(a1.x, hi.z, lo.z);
+      tc::split_tf32(a1.y, hi.w, lo.w);
+      const int off = r * 16 + kp * (TC_BM * 16);           // bytes: row r -> 16 B, K core matrix -> TC_BM*16 B
+      *reinterpret_cast<float4*>(tile + off) = hi;
+      *reinterpret_cast<float4*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
+    }
   }
 }
 
@@ -639,16 +719,18 @@ __global__ void k_tc_pack_a(GemmDesc d, float* __restrict__ out) {
 // Pre-split B operands (one per batch-local q, columns [0, n)) into the B' chunks the tensor-core
 // mainloop would build in shared memory: per (q, n-tile, 8-complex K-chunk) one contiguous block of
 // BP_FLOATS = [B^_hi ; B^_lo] rows in the canonical K-major UMMA layout (rows 2j = [Re b, -Im b],
-// 2j+1 = [Im b, Re b], rna TF32 split), zero outside k x n.  The GEMM then streams B with one bulk
-// async copy per chunk.  B(l, j) of batch q at B + q * b_stride + l * b_sk + j * b_sn.
+// 2j+1 = [Im b, Re b], round-to-nearest split, fp16 after the scale of *bmax or TF32), zero outside
+// k x n.  The GEMM then streams B with one bulk async copy per chunk.  B(l, j) of batch q at
+// B + q * b_stride + l * b_sk + j * b_sn.
 template <int BN>
 __global__ void k_tc_pack_b(const float2* __restrict__ B, int64_t b_stride, int64_t b_sk, int64_t b_sn, int k, int n,
-                            int nq, float* __restrict__ out) {
+                            int nq, float* __restrict__ out, const float* __restrict__ bmax) {
   using Cfg = TcGemmCfg<BN, 1>;
   constexpr int NR = Cfg::NR;
   const int nkc = (k + TC_BK - 1) / TC_BK;
   const int tiles_n = (n + BN - 1) / BN;
   const int64_t total = (int64_t)nq * tiles_n * nkc * BN * (TC_BK / 2);
+  const float s = (TC_F16 && bmax) ? tc::f16_scale(*bmax) : 1.f;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(e % BN);                 // column in tile (fastest)
     int64_t t = e / BN;
@@ -665,18 +747,42 @@ __global__ void k_tc_pack_b(const float2* __restrict__ B, int64_t b_stride, int6
       if (gk < k) b0 = Bq[(int64_t)gk * b_sk];
       if (gk + 1 < k) b1 = Bq[(int64_t)(gk + 1) * b_sk];
     }
-    float4 h0, l0, h1, l1;
-    tc::split_tf32(b0.x, h0.x, l0.x); tc::split_tf32(-b0.y, h0.y, l0.y);
-    tc::split_tf32(b1.x, h0.z, l0.z); tc::split_tf32(-b1.y, h0.w, l0.w);
-    tc::split_tf32(b0.y, h1.x, l1.x); tc::split_tf32(b0.x, h1.y, l1.y);
-    tc::split_tf32(b1.y, h1.z, l1.z); tc::split_tf32(b1.x, h1.w, l1.w);
-    float* blk = out + ((q * tiles_n + tn) * nkc + kc) * Cfg::BP_FLOATS;
-    const int off = (2 * j) * 4 + kp * (Cfg::LBO_B / 4);   // floats (the shared-memory B' layout)
-    *reinterpret_cast<float4*>(blk + off) = h0;
-    *reinterpret_cast<float4*>(blk + off + 4) = h1;
-    *reinterpret_cast<float4*>(blk + off + NR * 4) = l0;
-    *reinterpret_cast<float4*>(blk + off + NR * 4 + 4) = l1;
+    uint8_t* blk = reinterpret_cast<uint8_t*>(out + ((q * tiles_n + tn) * nkc + kc) * Cfg::BP_FLOATS);
+    if constexpr (TC_F16) {
+      uint2 h0, l0, h1, l1;
+      tc::split_f16x2(b0.x * s, -b0.y * s, h0.x, l0.x);
+      tc::split_f16x2(b1.x * s, -b1.y * s, h0.y, l0.y);
+      tc::split_f16x2(b0.y * s, b0.x * s, h1.x, l1.x);
+      tc::split_f16x2(b1.y * s, b1.x * s, h1.y, l1.y);
+      const int off = (2 * j) * 16 + (kp >> 1) * Cfg::LBO_B + (kp & 1) * 8;   // bytes
+      *reinterpret_cast<uint2*>(blk + off) = h0;
+      *reinterpret_cast<uint2*>(blk + off + 16) = h1;
+      *reinterpret_cast<uint2*>(blk + off + NR * 16) = l0;
+      *reinterpret_cast<uint2*>(blk + off + NR * 16 + 16) = l1;
+    } else {
+      float4 h0, l0, h1, l1;
+      tc::split_tf32(b0.x, h0.x, l0.x); tc::split_tf32(-b0.y, h0.y, l0.y);
+      tc::split_tf32(b1.x, h0.z, l0.z); tc::split_tf32(-b1.y, h0.w, l0.w);
+      tc::split_tf32(b0.y, h1.x, l1.x); tc::split_tf32(b0.x, h1.y, l1.y);
+      tc::split_tf32(b1.y, h1.z, l1.z); tc::split_tf32(b1.x, h1.w, l1.w);
+      const int off = (2 * j) * 16 + kp * Cfg::LBO_B;   // bytes (the shared-memory B' layout)
+      *reinterpret_cast<float4*>(blk + off) = h0;
+      *reinterpret_cast<float4*>(blk + off + 16) = h1;
+      *reinterpret_cast<float4*>(blk + off + NR * 16) = l0;
+      *reinterpret_cast<float4*>(blk + off + NR * 16 + 16) = l1;
+    }
   }
+}
+
+// ---------------------------------------------------------------- k_absmax
+// max(|Re x|, |Im x|) over a flat complex64 array, folded into *slot (the fp16 split's operand scale).
+__global__ void k_absmax(const float2* __restrict__ x, int64_t n, float* __restrict__ slot) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = x[i];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  tc::warp_absmax_to(m, slot);
 }
 
 }  // namespace fmmt

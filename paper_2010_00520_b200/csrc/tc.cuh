@@ -23,6 +23,7 @@
 // with R rows lives at byte (r*16) + (kk/4)*R*16 + (kk%4)*4.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace fmmt {
@@ -46,6 +47,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// Instruction descriptor: D f32, A/B f16 (kind::f16), both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -66,6 +71,14 @@ __device__ __forceinline__ void mma_tf32_el(uint32_t tmem_d, uint64_t a, uint64_
       "setp.ne.b32 p, %4, 0;\n\t"
       "elect.sync r|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_f16_el(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit_el(uint32_t bar_addr) {
@@ -171,6 +184,32 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
   hi = __uint_as_float(h);
   lo = __uint_as_float(l);
+}
+
+// x = hi + lo with hi, lo fp16 (round-to-nearest split of an already scaled value): 11 + 11
+// significant bits, as the TF32 split; packed as (hi bits, lo bits) halves of the two outputs.
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// Power-of-two operand scale for the fp16 split: |x| <= amax maps below 2^14 (fp16 max 65504),
+// the hi / lo parts keep 22 significant bits down to 2^-14 of that (3xFP16).
+__device__ __forceinline__ float f16_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(amax, &e);            // amax = f 2^e, f in [0.5, 1)
+  return ldexpf(1.f, 14 - e);  // amax * s < 2^14
+}
+
+// |re|, |im| maximum of a warp's values folded into *slot (positive floats order as their bits).
+__device__ __forceinline__ void warp_absmax_to(float m, float* slot) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(reinterpret_cast<int*>(slot), __float_as_int(m));
 }
 
 }  // namespace tc

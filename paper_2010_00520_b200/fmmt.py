@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmmt.so")
+# FMMT_LIB=tf32 selects the TF32-split build of the same sources (A/B measurement only)
+LIB_PATH = os.path.join(_HERE, "libfmmt_tf32.so" if os.environ.get("FMMT_LIB") == "tf32" else "libfmmt.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -112,3 +112,89 @@ def rel(a, b):
 def t_lib_to_math(buf: np.ndarray, n) -> np.ndarray:
     """Library operator slice layout [k][j][i] -> math (i, j, k)."""
     return np.reshape(np.asarray(buf).ravel(), n, order="F")
+
+
+class FromArrays:
+    """Factors given as the library's flat complex64 arrays (fmmt_op_import order and layout, e.g. from
+    fmmt_op_export of a GPU-compressed op), unpacked into the oracle's matrices (complex128 copies of the
+    same complex64 values) so that the oracle restores / translates from IDENTICAL factors
+    (BASELINE.json north_star: "identical compressed factors").  The GPU compressor itself is checked
+    separately against the oracle's T (error bound) and the oracle's ranks."""
+
+    def __init__(self, fmt: str, n, ndir: int, ranks, arrays):
+        self.fmt, self.n, self.ndir = fmt, tuple(n), ndir
+        n1, n2, n3 = self.n
+        a = [np.asarray(x).astype(np.complex128) for x in arrays]
+        F = lambda v, shape: np.reshape(v, shape, order="F")
+        rk = np.asarray(ranks, dtype=np.int64)
+        if fmt == "dense":
+            self.T = F(a[0], (n1, n2, n3, ndir))
+        elif fmt in ("tucker3d", "tt3d"):
+            rk = rk.reshape(ndir, -1)
+            self.parts = []
+            off = [0] * len(a)
+            for p in range(ndir):
+                if fmt == "tucker3d":
+                    r1, r2, r3 = rk[p]
+                    shapes = [(r1, r2, r3), (n1, r1), (n2, r2), (n3, r3)]
+                else:
+                    r1, r2 = rk[p]
+                    shapes = [(n1, r1), (r1, n2, r2), (n3, r2)]
+                part = []
+                for i, sh in enumerate(shapes):
+                    sz = int(np.prod(sh))
+                    part.append(F(a[i][off[i]:off[i] + sz], sh))
+                    off[i] += sz
+                self.parts.append(part)
+        elif fmt == "tucker4d":
+            r1, r2, r3, r4 = rk
+            self.core = F(a[0], (r1, r2, r3, r4))
+            self.U = [F(a[1], (n1, r1)), F(a[2], (n2, r2)), F(a[3], (n3, r3)), F(a[4], (ndir, r4))]
+        elif fmt == "htucker4d":
+            r1, r2, r3, r4, r12, r34 = rk
+            self.leaves = [F(a[0], (n1, r1)), F(a[1], (n2, r2)), F(a[2], (n3, r3)), F(a[3], (ndir, r4))]
+            self.c12, self.c34, self.c1234 = F(a[4], (r1, r2, r12)), F(a[5], (r3, r4, r34)), F(a[6], (r12, r34))
+        elif fmt == "tt4d":
+            r1, r2, r3 = rk
+            self.u1, self.c1, self.c2, self.ul = (F(a[0], (n1, r1)), F(a[1], (r1, n2, r2)), F(a[2], (r2, n3, r3)),
+                                                  F(a[3], (ndir, r3)))
+            self.t2 = restore.tt4d_t2(self.c2, self.ul)
+        else:
+            raise ValueError(fmt)
+        self._cache = {}
+
+    def restore(self, p: int) -> np.ndarray:
+        if p not in self._cache:
+            self._cache[p] = self._restore(p)
+        return self._cache[p]
+
+    def _restore(self, p: int) -> np.ndarray:
+        if self.fmt == "dense":
+            return self.T[..., p]
+        if self.fmt == "tucker3d":
+            c, u1, u2, u3 = self.parts[p]
+            return restore.tucker3d_restore(c, u1, u2, u3)
+        if self.fmt == "tt3d":
+            return restore.tt3d_restore(*self.parts[p])
+        if self.fmt == "tucker4d":
+            return restore.tucker4d_slice(self.core, self.U, p)
+        if self.fmt == "htucker4d":
+            return restore.htucker_slice(self.leaves, self.c12, self.c34, self.c1234, p)
+        return restore.tt4d_slice(self.u1, self.c1, self.c2, self.ul, p, self.t2)
+
+    def translate(self, sig_math: np.ndarray, p: int, i: int | None = None) -> np.ndarray:
+        """eq. (5) for direction p; sig_math row i (default p)."""
+        return translate.translate_fft(self.restore(p), sig_math[p if i is None else i])
+
+
+def rank_ok(gpu_r, ora_trunc, band=1e-9):
+    """Identical integer ranks, except inside the tie band of reading Q18 (oracle margin < band: r or r+1)."""
+    for g, tr in zip(gpu_r, ora_trunc):
+        if g != tr.rank and not (tr.margin < band and abs(int(g) - tr.rank) == 1):
+            return False
+    return True
+
+
+def lib_T(T4: np.ndarray) -> np.ndarray:
+    """Oracle T_4D (n1, n2, n3, ndir) -> the library's complex128 [ndir][n3][n2][n1] input layout."""
+    return np.ascontiguousarray(np.transpose(T4, (3, 2, 1, 0)))

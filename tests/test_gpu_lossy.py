@@ -11,7 +11,7 @@ import pytest
 from oracle import decomp, fmm, translate
 from synth import signature_seed, signatures
 
-from tests._helpers import Compressed, rel
+from tests._helpers import rank_ok, Compressed, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -79,9 +79,13 @@ def test_gpu_lossy_translate_and_ranks(fm, ctx, fmt):
     Td = torch.from_numpy(np.ascontiguousarray(np.transpose(T4, (3, 2, 1, 0)))).cuda()
     gop = ctx.compress(Td, cp.n, nd, fmt, tol)
     gr = gop.ranks()
+    # identical integer ranks, up to the tie band of reading Q18 (oracle margin < 1e-9: r or r+1)
     if fmt in ("tucker3d", "tt3d"):
-        ref = np.array(cp.ranks).ravel()
+        gr = gr.reshape(nd, -1)
+        for p in range(nd):
+            o = decomp.tucker_svd(T4[..., p], tol) if fmt == "tucker3d" else decomp.tt_svd(T4[..., p], tol)
+            assert rank_ok(gr[p], o.truncations), (p, gr[p], o.ranks)
     else:
-        ref = np.array(decomp.tucker_svd(T4, tol).ranks)
-    assert np.max(np.abs(gr - ref)) <= 1, (gr, ref)
+        o = decomp.tucker_svd(T4, tol)
+        assert rank_ok(gr, o.truncations), (gr, o.ranks)
     gop.close()

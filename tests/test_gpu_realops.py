@@ -1,0 +1,284 @@
+"""GPU parity on the REAL eq. (7) operators of configs 3-5, compressed on the GPU
+(the operators bench.py times), plus the export / virtual-sharding paths.
+
+What is checked, and against what (BASELINE.json north_star):
+  * integer ranks of the GPU compressor (Alg. 1/2/3) == the oracle's on
+    the oracle's own T, up to the tie band of reading Q18 (margins recorded);
+  * the GPU factors restore the ORACLE's T within the truncation bound (pins the
+    compressor's output to the oracle without feeding GPU data into it);
+  * identical-factor parity of the hot path: the GPU factors are exported
+    (fmmt_op_export) and the oracle restores (eqs. (8)-(14)) and translates (eq. (5))
+    from the same complex64 values; GPU restore <= 1e-6, translate <= 1e-5 relative
+    per direction on >= 16 directions per configuration;
+  * virtual direction sharding on one GPU: shards with dir_begin != 0 summed ==
+    the unsharded direction sum (eq. (6)), every format.
+Most cases are marked slow (oracle operators of up to 3.7 GB in complex128).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import decomp, fmm, translate
+from synth import config, signature_seed, signatures
+
+from tests._helpers import FromArrays, lib_T, operator, rank_ok, rel, t_lib_to_math
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TRANSLATE_TOL = 1e-5
+RESTORE_TOL = 1e-6
+MARGINS = {}
+
+
+@pytest.fixture(scope="module")
+def fm():
+    from paper_2010_00520_b200 import build
+    build.build()
+    from paper_2010_00520_b200 import fmmt
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return fmmt
+
+
+@pytest.fixture(scope="module")
+def ctx(fm):
+    c = fm.Context(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _report():
+    yield
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if os.path.isdir(out) and MARGINS:
+        with open(os.path.join(out, "realops_margins.json"), "w") as f:
+            json.dump(MARGINS, f, indent=1, sort_keys=True)
+
+
+def sample16(nd):
+    return sorted(set(np.linspace(0, nd - 1, 16).round().astype(int).tolist()))
+
+
+def gpu_translate(ctx, op, sig, N):
+    d_in = torch.from_numpy(sig).cuda()
+    d_out = torch.empty_like(d_in)
+    op.translate(d_in, d_out, sig.shape[0], N)
+    ctx.sync()
+    return d_out.cpu().numpy()
+
+
+def gpu_restore(ctx, op, p, n):
+    out = torch.empty(int(np.prod(n)), dtype=torch.complex64, device="cuda")
+    op.restore(p, out)
+    ctx.sync()
+    return t_lib_to_math(out.cpu().numpy(), n)
+
+
+def identical_factor_parity(ctx, op, fmt, cfg, dirs, key):
+    """Export the op's factors, oracle-restore / translate from them, compare with the GPU."""
+    c = config(cfg)
+    N = (c.Nx, c.Ny, c.Nz)
+    info = op.info()
+    nd = info["ndir"]
+    fa = FromArrays(fmt, info["n"], nd, op.ranks(), op.export())
+    sig = signatures(signature_seed(cfg, 0), nd, *N)
+    out = gpu_translate(ctx, op, sig, N)
+    sm, om = translate.sig_to_math(sig[dirs]), translate.sig_to_math(out[dirs])
+    werr_t = werr_r = 0.0
+    for i, p in enumerate(dirs):
+        werr_r = max(werr_r, rel(fa.restore(p), gpu_restore(ctx, op, p, info["n"])))
+        werr_t = max(werr_t, rel(translate.translate_fft(fa.restore(p), sm[i]), om[i]))
+    MARGINS[f"{key}/restore_err"] = werr_r
+    MARGINS[f"{key}/translate_err"] = werr_t
+    assert werr_r <= RESTORE_TOL, (key, "restore", werr_r)
+    assert werr_t <= TRANSLATE_TOL, (key, "translate", werr_t)
+
+
+def record_margins(key, truncs):
+    MARGINS[f"{key}/rank_margin_min"] = float(min(t.margin for t in truncs))
+
+
+# ------------------------------------------------------------------ export round trip (fast)
+@pytest.mark.parametrize("fmt,tol", [("tucker3d", 1e-4), ("tt3d", 1e-4), ("tucker4d", 1e-4), ("htucker4d", 1e-4),
+                                     ("tt4d", 1e-4), ("dense", 0.5)])
+def test_export_import_roundtrip(fm, ctx, fmt, tol):
+    """fmmt_op_export returns exactly the factors the op holds: re-importing them gives a
+    bit-identical matvec, and the exported sizes are the compressed_bytes count."""
+    c = config(2)
+    T4, _, _ = operator(2)
+    nd = T4.shape[3]
+    op = ctx.compress(lib_T(T4), c.n, nd, fmt, tol)
+    arrs = op.export()
+    info = op.info()
+    assert sum(a.size for a in arrs) * 8 == info["compressed_bytes"]
+    ranks = None if fmt == "dense" else op.ranks()
+    op2 = ctx.import_op(fmt, c.n, nd, ranks, arrs)
+    sig = signatures(signature_seed(2, 4), nd, c.Nx, c.Ny, c.Nz)
+    a = gpu_translate(ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+    b = gpu_translate(ctx, op2, sig, (c.Nx, c.Ny, c.Nz))
+    assert np.array_equal(a, b)
+    op.close()
+    op2.close()
+
+
+def test_export_errors(fm, ctx):
+    c = config(1)
+    T4, _, _ = operator(1)
+    op = ctx.compress(lib_T(T4), c.n, T4.shape[3], "tucker4d", 1e-4)
+    with pytest.raises(fm.FmmtError, match="E_ARG"):
+        fm._check(fm.fmmt_op_export(op.h, 5, None, 0, fm.C.byref(fm.C.c_int64())), op.ctx.h, "export")
+    small = np.zeros(1, np.complex64)
+    with pytest.raises(fm.FmmtError, match="E_ARG"):
+        fm._check(fm.fmmt_op_export(op.h, 0, small.ctypes.data, 1, fm.C.byref(fm.C.c_int64())), op.ctx.h, "export")
+    op.close()
+
+
+# ------------------------------------------------------------------ virtual sharding (fast)
+@pytest.mark.parametrize("fmt,tol", [("tucker3d", 1e-4), ("tt3d", 1e-4), ("tucker4d", 1e-4), ("htucker4d", 1e-4),
+                                     ("tt4d", 1e-4)])
+def test_virtual_sharding_sum(fm, ctx, fmt, tol):
+    """Three direction shards (dir_begin = 0, 113, 226 of 338) compressed and translated
+    separately on one GPU: the sum of the shards' direction sums equals the unsharded
+    direction sum (eq. (6)); 4D shards share the global ranks, 3D shards carry the
+    unsharded op's per-direction ranks."""
+    c = config(2)
+    T4, w, _ = operator(2)
+    nd = T4.shape[3]
+    N = (c.Nx, c.Ny, c.Nz)
+    Tl = torch.from_numpy(lib_T(T4)).cuda()
+    sig = torch.from_numpy(signatures(signature_seed(2, 5), nd, *N)).cuda()
+    wd = torch.from_numpy(w.astype(np.float32)).cuda()
+    full = ctx.compress(Tl, c.n, nd, fmt, tol)
+    ref = torch.empty(N[::-1], dtype=torch.complex64, device="cuda")
+    full.translate_sum(sig, torch.empty_like(sig), wd, ref, nd, N)
+    tot = torch.zeros_like(ref)
+    part = torch.empty_like(ref)
+    for r in range(3):
+        b, cnt = fm.shard_range(nd, r, 3)
+        sh = ctx.compress(Tl, c.n, nd, fmt, tol, b, cnt)
+        if fmt in ("tucker3d", "tt3d"):
+            assert np.array_equal(sh.ranks().reshape(cnt, -1), full.ranks().reshape(nd, -1)[b:b + cnt])
+        else:
+            assert np.array_equal(sh.ranks(), full.ranks())
+        s_in = sig[b:b + cnt].contiguous()
+        sh.translate_sum(s_in, torch.empty_like(s_in), wd[b:b + cnt].contiguous(), part, cnt, N)
+        ctx.sync()
+        tot += part
+        sh.close()
+    ctx.sync()
+    e = rel(ref.cpu().numpy(), tot.cpu().numpy())
+    MARGINS[f"shard3/{fmt}"] = e
+    assert e <= 1e-5, e
+    full.close()
+
+
+# ------------------------------------------------------------------ config 3 (elongated grid), all 338 directions
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["tucker3d", "tt3d"])
+def test_cfg3_real_operator(fm, ctx, fmt):
+    c = config(3)
+    tol = 1e-5
+    T4, _, _ = operator(3)
+    nd = T4.shape[3]
+    op = ctx.compress(lib_T(T4), c.n, nd, fmt, tol)
+    gr = op.ranks().reshape(nd, -1)
+    worst = 1.0
+    for p in range(nd):
+        o = decomp.tucker_svd(T4[..., p], tol) if fmt == "tucker3d" else decomp.tt_svd(T4[..., p], tol)
+        assert rank_ok(gr[p], o.truncations), (p, gr[p], o.ranks)
+        worst = min(worst, min(t.margin for t in o.truncations))
+    MARGINS[f"cfg3/{fmt}/rank_margin_min"] = worst
+    # the GPU factors restore the oracle's T within the per-direction truncation bound
+    for p in sample16(nd):
+        assert rel(T4[..., p], gpu_restore(ctx, op, p, c.n)) <= tol * (1 + 1e-3) + 2e-6, p
+    identical_factor_parity(ctx, op, fmt, 3, sample16(nd), f"cfg3/{fmt}")
+    op.close()
+
+
+# ------------------------------------------------------------------ config 4 (64^3, 882 directions), 4D formats
+@pytest.fixture(scope="module")
+def cfg4_T():
+    T4, _, _ = operator(4)
+    return T4
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["tucker4d", "htucker4d"])
+def test_cfg4_real_operator(fm, ctx, cfg4_T, fmt):
+    c = config(4)
+    tol = 1e-4
+    T4 = cfg4_T
+    nd = T4.shape[3]
+    o = decomp.tucker_svd(T4, tol) if fmt == "tucker4d" else decomp.htucker_svd(T4, tol)
+    op = ctx.compress(lib_T(T4), c.n, nd, fmt, tol)
+    gr = op.ranks()
+    assert rank_ok(gr, o.truncations), (gr, o.ranks)
+    record_margins(f"cfg4/{fmt}", o.truncations)
+    del o
+    # global truncation bound (reading Q16) on a 16-direction sample of the oracle's T
+    num = den = 0.0
+    for p in sample16(nd):
+        got = gpu_restore(ctx, op, p, c.n)
+        num += np.linalg.norm((got - T4[..., p]).ravel()) ** 2
+        den += np.linalg.norm(T4[..., p].ravel()) ** 2
+    assert np.sqrt(num / den) <= 2 * tol + 2e-6
+    identical_factor_parity(ctx, op, fmt, 4, sample16(nd), f"cfg4/{fmt}")
+    op.close()
+
+
+# ------------------------------------------------------------------ config 5 (128x128x64, 882 directions)
+@pytest.mark.slow
+def test_cfg5_tucker3d_ranks_sample(fm, ctx):
+    """Tucker-3D ranks of the GPU compressor == the oracle's on 16 sampled directions of the
+    oracle's config-5 operator (1M-point slices)."""
+    c = config(5)
+    tol = 1e-4
+    khat, _, _, _ = fmm.direction_grid(c.L, c.nphi)
+    grid = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L)
+    dirs = sample16(c.ndir)
+    Ts = np.stack([fmm.fft_operator_3d(grid, khat[p]) for p in dirs], axis=-1)
+    op = ctx.compress(lib_T(Ts), c.n, len(dirs), "tucker3d", tol)
+    gr = op.ranks().reshape(len(dirs), -1)
+    worst = 1.0
+    for i in range(len(dirs)):
+        o = decomp.tucker_svd(Ts[..., i], tol)
+        assert rank_ok(gr[i], o.truncations), (dirs[i], gr[i], o.ranks)
+        worst = min(worst, min(t.margin for t in o.truncations))
+        assert rel(Ts[..., i], gpu_restore(ctx, op, i, c.n)) <= tol * (1 + 1e-3) + 2e-6
+    MARGINS["cfg5/tucker3d/rank_margin_min"] = worst
+    op.close()
+
+
+@pytest.mark.slow
+def test_cfg5_bench_operators(fm, ctx):
+    """The operators bench.py times at config 5 (eq. (7) built on the GPU in FP64, all 882
+    directions, GPU-compressed TT-4D and Tucker-3D at 1e-4): their restorations bound the
+    oracle's T on 16 directions, and the hot path matches the oracle on the exported factors."""
+    c = config(5)
+    tol = 1e-4
+    khat, _ = fm.direction_grid(c.L, c.nphi)
+    T = torch.empty((c.ndir,) + c.n[::-1], dtype=torch.complex128, device="cuda")
+    ctx.build_operator(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L, khat, T)
+    ops = {f: ctx.compress(T, c.n, c.ndir, f, tol) for f in ("tt4d", "tucker3d")}
+    del T
+    torch.cuda.empty_cache()
+    okhat, _, _, _ = fmm.direction_grid(c.L, c.nphi)
+    grid = fmm.OperatorGrid(c.Nx, c.Ny, c.Nz, c.edge, c.k, c.L)
+    dirs = sample16(c.ndir)
+    num = den = 0.0
+    for p in dirs:
+        Tp = fmm.fft_operator_3d(grid, okhat[p])
+        e3 = rel(Tp, gpu_restore(ctx, ops["tucker3d"], p, c.n))
+        assert e3 <= tol * (1 + 1e-3) + 2e-6, (p, e3)
+        got = gpu_restore(ctx, ops["tt4d"], p, c.n)
+        num += np.linalg.norm((got - Tp).ravel()) ** 2
+        den += np.linalg.norm(Tp.ravel()) ** 2
+    assert np.sqrt(num / den) <= 2 * tol + 2e-6
+    MARGINS["cfg5/tt4d/ranks"] = [int(x) for x in ops["tt4d"].ranks()]
+    for f, op in ops.items():
+        identical_factor_parity(ctx, op, f, 5, dirs, f"cfg5/{f}")
+        op.close()
