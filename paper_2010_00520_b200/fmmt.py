@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -163,9 +164,12 @@ class Context:
         _check(st, None, "fmmt_init")
         self.h = h
         self.device, self.rank, self.world = device, rank, world
+        self._ops = weakref.WeakSet()     # live ops: destroyed before the context (they reference it)
 
     def close(self):
         if self.h:
+            for op in list(self._ops):
+                op.close()
             fmmt_destroy(self.h)
             self.h = None
 
@@ -251,6 +255,7 @@ class Context:
 class Op:
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
+        ctx._ops.add(self)
 
     def close(self):
         if self.h:

@@ -299,8 +299,9 @@ def test_error_codes(fm, ctx):
 
 
 def test_single_direction_and_batching_invariance(fm, ctx):
-    """ndir = 1 and every batch size give bit-identical outputs (the batch
-    split only changes which directions share a launch)."""
+    """ndir = 1 and every batch size give the same outputs: the batch split only changes which
+    directions share a launch, and the per-batch power-of-two operand scales of the fp16 split
+    (DESIGN 6.1), i.e. the rounding, so batchings agree to 1e-6 relative per direction."""
     c = config(2)
     cp = compressed(2, "tucker4d", 1e-4)
     sig = signatures(signature_seed(2, 3), cp.ndir, c.Nx, c.Ny, c.Nz)
@@ -308,7 +309,8 @@ def test_single_direction_and_batching_invariance(fm, ctx):
     ref = run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz))
     for b in (1, 7, 338):
         op.set_batch(b)
-        assert np.array_equal(run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz)), ref)
+        got = run_translate(fm, ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+        assert max(rel(ref[p], got[p]) for p in range(cp.ndir)) <= 1e-6
     op.close()
     # single direction (U4 row subset)
     arrays = list(cp.arrays)
