@@ -54,13 +54,14 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def restore_peak_tflops(peaks, burst=True):
-    """FP32-accurate restore peak of the tensor cores (SURVEY §8(d) P_restore): the kernels run
-    kind::tf32 with the 3xTF32 split (3 MMAs per useful MAC).  TF32 dense = bf16 dense x 1/2 (the
-    guide's nominal ratio 1.1 / 2.25 PF), bf16 = the measured cuBLAS figure (burst: a pass of the
-    step timed at max clocks; sustained: the seconds-long power-capped figure)."""
+def restore_peak_tflops(peaks, burst=True, split="fp16"):
+    """FP32-accurate restore peak of the tensor cores (SURVEY §8(d) P_restore: the best unit's
+    FP32-accurate rate).  The restore contractions run 3 tensor MMAs per useful MAC (hi.hi + hi.lo +
+    lo.hi of an 11 + 11-bit split): fp16 split (kind::f16, the product build) at the fp16 = bf16 dense
+    rate, or TF32 split (kind::tf32, A/B build) at bf16 x 1/2 (the guide's nominal 1.1 / 2.25 PF).
+    bf16 = the measured cuBLAS figure: burst (a pass timed at max clocks) or sustained."""
     bf16 = float(peaks.get("bf16_tflops") if burst else peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    return bf16 * 0.5 / 3.0
+    return bf16 * (1.0 if split == "fp16" else 0.5) / 3.0
 
 
 # ------------------------------------------------------------------ algorithmic work (SURVEY §8(d))
@@ -104,7 +105,7 @@ def restore_cmac_per_dir(fmt, n, r):
     raise ValueError(fmt)
 
 
-def op_roofline(fmt, info, ranks, ndir_local, peaks, burst=True):
+def op_roofline(fmt, info, ranks, ndir_local, peaks, burst=True, split="fp16"):
     """t_roof = max((B_sig + B_fac)/BW, F_restore/P_restore) for one matvec of one op,
     B_fft = 0 (the half-padded spectra of a batch stay in L2 / on chip by design)."""
     n = info["n"]
@@ -117,7 +118,7 @@ def op_roofline(fmt, info, ranks, ndir_local, peaks, burst=True):
     b_sig = 16.0 * K * ndir_local
     b_fac = float(info["compressed_bytes"])
     bw = float(peaks["hbm_gbs"]) * 1e9
-    p = restore_peak_tflops(peaks, burst) * 1e12
+    p = restore_peak_tflops(peaks, burst, split) * 1e12
     t_hbm, t_fl = (b_sig + b_fac) / bw, 8.0 * cmac / p
     return {"t_roof_ms": 1e3 * max(t_hbm, t_fl), "t_hbm_ms": 1e3 * t_hbm, "t_restore_ms": 1e3 * t_fl,
             "bound": "tensor" if t_fl > t_hbm else "hbm", "restore_gflop": 8.0 * cmac / 1e9,
@@ -491,7 +492,7 @@ def far_matvec_measure(run, ops, cfg, cfg_index, d0, dn, wd, N, flush):
                     "synthetic sphere-shell basis functions, CN(0,1) patterns drawn on the device"}
 
 
-def summarize(res, world, peaks, peak_src):
+def summarize(res, world, peaks, peak_src, split="fp16"):
     """Value, per-op and step-level roofline, dominant-kernel roofline."""
     cfg_ops = res["ops"]
     dn = res["dn"]
@@ -504,7 +505,7 @@ def summarize(res, world, peaks, peak_src):
         npad = info["n"][0] * info["n"][1] * info["n"][2]
         units = ndir_total * npad
         total_units += units
-        rf = op_roofline(fmt, info, ranks, dn, peaks, burst=True)
+        rf = op_roofline(fmt, info, ranks, dn, peaks, burst=True, split=split)
         troof += rf["t_roof_ms"]
         ms = float(res["per_op"][i])
         d = {"ms": round(ms, 4), "gpt_s": round(units / (ms * 1e-3) / 1e9, 3), "rank_max": info["rank_max"],
@@ -521,8 +522,10 @@ def summarize(res, world, peaks, peak_src):
     out = {"value": round(value, 3), "ms_per_step": round(t_step, 4), "per_format": per_format,
            "step_roofline": {"t_roof_ms": round(troof, 4), "t_ms": round(t_step, 4), "frac": round(troof / t_step, 4),
                              "definition": "sum over ops of max((B_sig+B_fac)/BW, F_restore/P_restore), cheapest "
-                                           "contraction order, P_restore = measured bf16 burst x 0.5 (TF32) / 3 "
-                                           "(3xTF32), BW = measured HBM copy (SURVEY 8(d))"},
+                                           "contraction order, P_restore = measured bf16 burst / 3 (3 fp16 MMAs per "
+                                           "FP32-accurate MAC; x 0.5 for the TF32-split build), BW = measured HBM copy "
+                                           "(SURVEY 8(d))",
+                             "p_restore_tflops": round(restore_peak_tflops(peaks, True, split), 1)},
            "gpu_launches": res["launches"], "clocks": res["clocks"], "setup_s": res["setup_s"]}
     if "dense_ms" in res:
         dms = res["dense_ms"]
@@ -549,8 +552,8 @@ def summarize(res, world, peaks, peak_src):
         if cand:
             dname, (dms, dl) = max(cand.items(), key=lambda kv: kv[1][0])
             ach = kfl[dname] / (dms * 1e-3) / 1e12
-            pk = restore_peak_tflops(peaks, burst=True)
-            pks = restore_peak_tflops(peaks, burst=False)
+            pk = restore_peak_tflops(peaks, burst=True, split=split)
+            pks = restore_peak_tflops(peaks, burst=False, split=split)
             traffic = None
             tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(tp):
@@ -561,8 +564,10 @@ def summarize(res, world, peaks, peak_src):
             out["roofline"] = {"bound": "tensor", "kernel": dname, "achieved": round(ach, 3), "peak": round(pk, 2),
                                "unit": "TFLOP/s", "frac": round(ach / pk, 4), "traffic": traffic,
                                "frac_of_sustained": round(ach / pks, 4),
-                               "peak_source": f"{peak_src}: bf16 burst {peaks.get('bf16_tflops')} x 0.5 (TF32, guide's "
-                                              f"nominal ratio) / 3 (3xTF32 split) = {pk:.1f} TFLOP/s",
+                               "peak_source": (f"{peak_src}: bf16 burst {peaks.get('bf16_tflops')} / 3 (3 fp16 MMAs per "
+                                               f"FP32-accurate MAC; fp16 rate = bf16) = {pk:.1f} TFLOP/s") if split == "fp16"
+                                              else (f"{peak_src}: bf16 burst {peaks.get('bf16_tflops')} x 0.5 (TF32, guide's "
+                                                    f"nominal ratio) / 3 (3xTF32 split) = {pk:.1f} TFLOP/s"),
                                "work": "cheapest-order a4 contraction flops of the kernel (8 per complex MAC), "
                                        "FFT / Hadamard ALU work excluded; CUDA events on the launching stream"}
     return out
@@ -581,7 +586,8 @@ def run_ours(args):
         if run.rank == 0:
             print(json.dumps({"quick": True, "ms_per_step": res["t_step"], "launches": res["launches"]}), flush=True)
         return
-    head = summarize(res, run.world, peaks, peak_src)
+    split = run.fmmt.SPLIT
+    head = summarize(res, run.world, peaks, peak_src, split)
     ndir = cfg.ndir
     total_units = sum(ndir * info["n"][0] * info["n"][1] * info["n"][2] for _, _, info, _ in res["ops"])
     e2e_value = total_units / (res["e2e_t"] * 1e-3) / 1e9
@@ -593,7 +599,7 @@ def run_ours(args):
                 continue
             c2 = get_config(ci)
             r2, _, _ = run.measure(ci, list(c2.formats), max(3, args.steps // 2), 3, full=False)
-            s2 = summarize(r2, 1, peaks, peak_src)
+            s2 = summarize(r2, 1, peaks, peak_src, split)
             others[f"config{ci}"] = {"workload": r2["workload"], **{k: s2[k] for k in (
                 "value", "ms_per_step", "step_roofline", "roofline", "per_format", "dense", "gpu_launches", "setup_s")
                 if k in s2}, "unit": UNIT, "kernels_top": dict(list(s2.get("kernels", {}).items())[:8])}
@@ -619,7 +625,8 @@ def run_ours(args):
         "config": {"workload": res["workload"],
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": f"direction-shard x{run.world}",
-                   "restore_gemm": {"tc": "tcgen05 kind::tf32, 3xTF32 split, FP32 accumulate",
+                   "restore_gemm": {"tc": f"tcgen05 kind::{'f16' if split == 'fp16' else 'tf32'}, 3-product "
+                                          f"{split} hi/lo split, FP32 accumulation, packed-operand pipeline",
                                     "ffma": "FP32 FFMA"}[args.gemm]},
         "gpu_launches": head["gpu_launches"],
         "roofline": head.get("roofline"),

@@ -30,6 +30,7 @@
 #include "kernels_fft.cuh"
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
+#include "kernels_tcpk.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -225,11 +226,14 @@ struct GemmLaunch {
   const char* name = "";
   // pre-split the (dynamic) B operand of descriptor `first` into pack_dst before the launch
   float* pack_dst = nullptr;
+  // pre-split the (dynamic) A operands of the launch's descriptors into their Ap before the launch
+  bool pack_a_dyn = false;
 };
 
 struct Batch {
   int q0 = 0, nq = 0;
   std::vector<GemmLaunch> gemms;
+  int zp_first = -1, zp_n = 0;   // z-stage: descriptors packing this batch's G_q (k_pk_pack_a_multi)
 };
 
 struct fmmt_op {
@@ -247,7 +251,6 @@ struct fmmt_op {
   float2* E = nullptr;                         // H-Tucker: (C12 . C1234) x1 U1 x2 U2, n1 n2 x r34
   float* tbar1_pk = nullptr;                   // T1 pre-split for the tensor-core z-stage (k_tc_pack_a)
   float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
-  std::vector<float*> arr_pk;                  // per factor array: pre-split copy (static slice-GEMM A operands)
   int64_t w_ncomp = 1;                         // signature components W is allocated for
   float2* zscr = nullptr;                      // n3 = 64 tensor-core z-stage: even-pass partials (batch)
   int64_t zscr_elems = 0;
@@ -278,14 +281,23 @@ struct fmmt_op {
   // at the start of every matvec; the producing GEMM folds its max |C| in, the consumer derives its scale)
   float* d_slots = nullptr;
   int64_t nslots_dyn = 0;
+  // packed-operand pipeline (kernels_tcpk.cuh): dynamic A workspaces per launch position of a batch,
+  // the z-stage's packed G_q (per batch-local q) and packed static V factors (per direction p)
+  std::vector<float*> apk_dyn;
+  float* gpk = nullptr;
+  int64_t gp_stride = 0;
+  float* vpk_static = nullptr;
+  int64_t* d_vp_off = nullptr;
+  int64_t vp_stride = 0;
+  bool packed = false;                         // finalize_packs ran for the tensor-core pipeline
+  fmmt::PkB* d_vitems = nullptr;               // TT-4D: pack items of the batch's V_q (per q [, parity])
+  int64_t nvitems = 0;
+  std::vector<std::pair<std::vector<int64_t>, float*>> pk_cache;   // static operand packs (key -> buffer)
   // host staging for translate_sum_host
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
   float2* d_sum_host = nullptr;
   // far-field matvec (fmmt_far_matvec): aggregated and translated signatures [ndir][ncomp][K]
-  std::vector<float*> bpk_static;               // pre-split static B operands of the slice GEMMs (per batch)
-  float* Mpk = nullptr;                         // H-Tucker G GEMM: pre-split M_q of a batch
-  int64_t mpk_floats = 0;
   float* Vpk = nullptr;                         // TT-4D z-stage: pre-split V_q of a batch (k_tc_pack_b)
   int64_t vpk_floats = 0;
   float2 *fA = nullptr, *fB = nullptr, *fPart = nullptr;   // + disaggregation partials [nsplit][N]
@@ -499,81 +511,6 @@ static fmmt_status pack_a(fmmt_op* op, const GemmDesc& d, float** out) {
   return FMMT_OK;
 }
 
-// A descriptor whose A operand is factor array `ai` (static): attach the pre-split copy
-// (made once per op; skipped when packing is disabled or the kernel is not tcgen05).
-static fmmt_status with_packed_a(fmmt_op* op, int ai, GemmDesc& d) {
-  if (!op->ctx->pack_factors || op->ctx->gemm_impl != 1) return FMMT_OK;
-  if ((int)op->arr_pk.size() <= ai) op->arr_pk.resize(ai + 1, nullptr);
-  if (!op->arr_pk[ai]) {
-    fmmt_status st = pack_a(op, d, &op->arr_pk[ai]);
-    if (st) return st;
-  }
-  d.Ap = op->arr_pk[ai];
-  d.a_nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
-  return FMMT_OK;
-}
-
-// Pre-split B of a tensor-core descriptor (k_tc_pack_b with the launch's BN): floats needed and the launch.
-static int tc_bn_for(int64_t n) { return n >= 32 ? 32 : 16; }   // as add_gemm picks it (single-descriptor groups)
-
-static int64_t packb_floats(const GemmDesc& d) {
-  const int bn = tc_bn_for(d.n);
-  const int64_t nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (d.n + bn - 1) / bn;
-  return (int64_t)d.batch * tiles_n * nkc * (64 * bn * fmmt::TC_ESZ / 4);   // BP_FLOATS = 64 BN (tf32) / 32 BN (f16)
-}
-
-static fmmt_status launch_pack_b(fmmt_ctx* ctx, const GemmDesc& d, float* out) {
-  // (d.bmax: the scale slot of B, set by the plan)
-  const int bn = tc_bn_for(d.n);
-  const int64_t items = packb_floats(d) / (64 * bn) * bn * (fmmt::TC_BK / 2);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16));
-  ProfScope ps(ctx, "pack_b");
-  if (bn == 32)
-    fmmt::k_tc_pack_b<32><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out, d.bmax);
-  else
-    fmmt::k_tc_pack_b<16><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, d.batch, out, d.bmax);
-  FMMT_CUDA(ctx, cudaGetLastError());
-  return FMMT_OK;
-}
-
-// A descriptor whose B operand is static (factor rows of this batch): pre-split it once per op (synchronous).
-static fmmt_status with_packed_b_static(fmmt_op* op, GemmDesc& d) {
-  fmmt_ctx* ctx = op->ctx;
-  if (!ctx->pack_b || ctx->gemm_impl != 1 || !d.Ap) return FMMT_OK;
-  float* buf = nullptr;
-  const int64_t floats = packb_floats(d);
-  if (fmmt_status st = dev_alloc(op, &buf, floats * 4, MEM_DERIVED, "pre-split B")) return st;
-  op->bpk_static.push_back(buf);
-  if (fmmt_status st = launch_pack_b(ctx, d, buf)) return st;
-  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  d.Bp = buf;
-  return FMMT_OK;
-}
-
-// A per-direction descriptor whose A and B are both static factors (Tucker-3D mode-1: core_p, U1_p;
-// TT-3D head: C1_p, U1_p): pre-split both once per op (asynchronous; build_plans synchronises).
-static fmmt_status with_packed_static(fmmt_op* op, GemmDesc& d) {
-  fmmt_ctx* ctx = op->ctx;
-  if (!ctx->pack_b || !ctx->pack_factors || ctx->gemm_impl != 1) return FMMT_OK;
-  const int64_t tiles_m = (d.m + fmmt::TC_BM - 1) / fmmt::TC_BM, nkc = (d.k + fmmt::TC_BK - 1) / fmmt::TC_BK;
-  const int64_t fa = tiles_m * nkc * fmmt::TC_PACK_FLOATS, fb = packb_floats(d);
-  float* buf = nullptr;
-  if (fmmt_status st = dev_alloc(op, &buf, (fa + fb) * 4, MEM_DERIVED, "pre-split operands")) return st;
-  op->bpk_static.push_back(buf);
-  {
-    ProfScope ps(ctx, "pack_a");
-    const int64_t work = tiles_m * fmmt::TC_BM * nkc * (fmmt::TC_BK / 2);
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 16));
-    fmmt::k_tc_pack_a<<<blocks, 256, 0, ctx->stream>>>(d, buf);
-    FMMT_CUDA(ctx, cudaGetLastError());
-  }
-  if (fmmt_status st = launch_pack_b(ctx, d, buf + fa)) return st;
-  d.Ap = buf;
-  d.a_nkc = (int)nkc;
-  d.Bp = buf + fa;
-  return FMMT_OK;
-}
-
 // Tucker chain shared by the Tucker / H-Tucker formats: per batch-local q with
 // 3D core at core_q, H_q = U1 . core_q(1), G_q[:,:,c] = H_q[:,:,c] . U2^T.
 static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
@@ -596,7 +533,6 @@ static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
       d1.amax = sslot(op, 0);
       d1.bmax = sslot(op, 1);
       d1.cmax = dslot(op, bi, 0);
-      if (fmmt_status st = with_packed_static(op, d1)) return st;
       sa.push_back(d1);
       GemmDesc d2 = gdx(Hq, U2, Gq, n1 * r3, n2, r2, r2 * r3, r2, n1, 1, n2, 1, 1, n12, n1, n1);
       d2.amax = dslot(op, bi, 0);
@@ -628,19 +564,293 @@ static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
 }
 
 static fmmt_status ensure_zscr(fmmt_op* op);
+static void fill_zargs(fmmt_op* op, ZArgs& a, int bi);
+
+// ---------------------------------------------------------------- packed operands (kernels_tcpk.cuh)
+// Every tensor-core contraction streams both operands pre-split (fp16 / TF32 hi + lo, UMMA layout):
+//   static operands (factors, T1, E; the rows of the direction factor a batch uses) are packed once per
+//   op at plan time, dynamic ones (intermediates a batch produces) by a pack launch right before their
+//   consumer, into per-launch-position workspaces shared by all batches.
+static bool in_mem(const fmmt_op* op, const void* p, int kind_a, int kind_b) {
+  const char* c = (const char*)p;
+  for (auto& kv : op->mem)
+    if ((kv.second.second == kind_a || kv.second.second == kind_b) && c >= (const char*)kv.first &&
+        c < (const char*)kv.first + kv.second.first)
+      return true;
+  return false;
+}
+static bool is_static_operand(const fmmt_op* op, const void* p) { return in_mem(op, p, MEM_FACTOR, MEM_DERIVED); }
+
+static int64_t pk_a_floats_sub(const GemmDesc& d) {
+  return ((d.m + fmmt::TC_BM - 1) / fmmt::TC_BM) * ((d.k + fmmt::TC_BK - 1) / fmmt::TC_BK) * fmmt::TC_PACK_FLOATS;
+}
+static int64_t pk_b_floats_sub(const GemmDesc& d, int bn) {
+  return ((d.n + bn - 1) / bn) * ((d.k + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
+}
+
+static fmmt_status launch_pack_a_multi(fmmt_ctx* ctx, const GemmDesc* d_descs, int ndesc, int64_t max_items) {
+  if (ndesc <= 0) return FMMT_OK;
+  const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((max_items + 255) / 256, (int64_t)ctx->num_sms * 8));
+  ProfScope ps(ctx, "pack_a");
+  fmmt::k_pk_pack_a_multi<<<dim3(bx, (unsigned)ndesc), 256, 0, ctx->stream>>>(d_descs);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+static fmmt_status launch_pack_b_bn(fmmt_ctx* ctx, const GemmDesc& d, int bn, float* out) {
+  const int nb = d.sB == 0 ? 1 : d.batch;
+  const int64_t items = (int64_t)nb * pk_b_floats_sub(d, bn) / (64 * bn * fmmt::TC_ESZ / 4) * bn * (fmmt::TC_BK / 2);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16));
+  ProfScope ps(ctx, "pack_b");
+  if (bn == 32)
+    fmmt::k_tc_pack_b<32><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, nb, out, d.bmax);
+  else
+    fmmt::k_tc_pack_b<16><<<grid, 256, 0, ctx->stream>>>(d.B, d.sB, d.b_sk, d.b_sn, d.k, d.n, nb, out, d.bmax);
+  FMMT_CUDA(ctx, cudaGetLastError());
+  return FMMT_OK;
+}
+
+// Static A of d: packed once (cached by operand addressing), d.Ap / a_nkc / a_pk_sub set.
+static fmmt_status pack_static_a(fmmt_op* op, GemmDesc& d) {
+  fmmt_ctx* ctx = op->ctx;
+  const int nb = d.sA == 0 ? 1 : d.batch;
+  std::vector<int64_t> key = {0, (int64_t)d.A, d.m, d.k, d.a_s0, d.a_s1, d.a_div, d.a_sk, d.sA, nb};
+  float* buf = nullptr;
+  for (auto& e : op->pk_cache)
+    if (e.first == key) buf = e.second;
+  const int64_t sub = pk_a_floats_sub(d);
+  if (!buf) {
+    if (fmmt_status st = dev_alloc(op, &buf, nb * sub * 4, MEM_DERIVED, "packed A")) return st;
+    GemmDesc t = d;
+    t.Ap = buf;
+    t.a_pk_sub = sub;
+    t.batch = nb;
+    GemmDesc* dd = nullptr;
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&dd, sizeof(GemmDesc), ctx->stream));
+    FMMT_CUDA(ctx, cudaMemcpyAsync(dd, &t, sizeof(GemmDesc), cudaMemcpyHostToDevice, ctx->stream));
+    fmmt_status st = launch_pack_a_multi(ctx, dd, 1, nb * sub / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * (fmmt::TC_BK / 2));
+    cudaFreeAsync(dd, ctx->stream);
+    if (st) return st;
+    op->pk_cache.push_back({key, buf});
+  }
+  d.Ap = buf;
+  d.a_nkc = (int)((d.k + fmmt::TC_BK - 1) / fmmt::TC_BK);
+  d.a_pk_sub = d.sA == 0 ? 0 : sub;
+  return FMMT_OK;
+}
+
+// Static B of d for a launch with bn columns per tile: packed once (cached), d.Bp / b_pk_sub set.
+static fmmt_status pack_static_b(fmmt_op* op, GemmDesc& d, int bn) {
+  const int nb = d.sB == 0 ? 1 : d.batch;
+  std::vector<int64_t> key = {1, (int64_t)d.B, d.n, d.k, d.b_sk, d.b_sn, d.sB, nb, bn};
+  float* buf = nullptr;
+  for (auto& e : op->pk_cache)
+    if (e.first == key) buf = e.second;
+  const int64_t sub = pk_b_floats_sub(d, bn);
+  if (!buf) {
+    if (fmmt_status st = dev_alloc(op, &buf, nb * sub * 4, MEM_DERIVED, "packed B")) return st;
+    if (fmmt_status st = launch_pack_b_bn(op->ctx, d, bn, buf)) return st;
+    op->pk_cache.push_back({key, buf});
+  }
+  d.Bp = buf;
+  d.b_pk_sub = d.sB == 0 ? 0 : sub;
+  return FMMT_OK;
+}
+
+// After the batches are planned: pack every static operand, give every dynamic one a workspace region
+// (its launch packs it), and prepare the z-stage's packed G (dynamic) and V (static) operands.
+static fmmt_status finalize_packs(fmmt_op* op) {
+  fmmt_ctx* ctx = op->ctx;
+  op->packed = false;
+  if (ctx->gemm_impl != 1 || op->format == FMMT_DENSE) return FMMT_OK;
+  fmmt_status st;
+  // ---- GEMM launches
+  size_t npos = 0;
+  for (auto& b : op->batches) npos = std::max(npos, b.gemms.size());
+  std::vector<int64_t> need(npos, 0), needb(npos, 0);
+  for (auto& b : op->batches)
+    for (size_t li = 0; li < b.gemms.size(); ++li) {
+      const GemmLaunch& L = b.gemms[li];
+      int64_t a = 0, bb = 0;
+      for (int i = 0; i < L.ndesc; ++i) {
+        const GemmDesc& d = op->descs[L.first + i];
+        if (!d.Ap && !is_static_operand(op, d.A)) a += (d.sA == 0 ? 1 : d.batch) * pk_a_floats_sub(d);
+        if (!d.Bp && !is_static_operand(op, d.B)) bb += (d.sB == 0 ? 1 : d.batch) * pk_b_floats_sub(d, L.tc_bn);
+      }
+      need[li] = std::max(need[li], a);
+      needb[li] = std::max(needb[li], bb);
+    }
+  for (auto& p : op->apk_dyn) dev_free(op, p);
+  op->apk_dyn.assign(2 * npos, nullptr);
+  for (size_t li = 0; li < npos; ++li) {
+    if (need[li] && (st = dev_alloc(op, &op->apk_dyn[li], need[li] * 4, MEM_WORKSPACE, "packed A workspace"))) return st;
+    if (need[li]) FMMT_CUDA(ctx, cudaMemsetAsync(op->apk_dyn[li], 0, need[li] * 4, ctx->stream));   // padding stays 0
+    if (needb[li] && (st = dev_alloc(op, &op->apk_dyn[npos + li], needb[li] * 4, MEM_WORKSPACE, "packed B workspace")))
+      return st;
+  }
+  for (auto& b : op->batches)
+    for (size_t li = 0; li < b.gemms.size(); ++li) {
+      GemmLaunch& L = b.gemms[li];
+      int64_t ao = 0, bo = 0;
+      for (int i = 0; i < L.ndesc; ++i) {
+        GemmDesc& d = op->descs[L.first + i];
+        if (!d.Ap) {
+          if (is_static_operand(op, d.A)) {
+            if ((st = pack_static_a(op, d))) return st;
+          } else {
+            const int64_t sub = pk_a_floats_sub(d);
+            d.Ap = op->apk_dyn[li] + ao;
+            d.a_nkc = (int)((d.k + fmmt::TC_BK - 1) / fmmt::TC_BK);
+            d.a_pk_sub = d.sA == 0 ? 0 : sub;
+            ao += (d.sA == 0 ? 1 : d.batch) * sub;
+            L.pack_a_dyn = true;
+          }
+        } else if (d.a_pk_sub == 0 && d.sA != 0 && d.batch > 1) {
+          d.a_pk_sub = pk_a_floats_sub(d);
+        }
+        if (!d.Bp) {
+          if (is_static_operand(op, d.B)) {
+            if ((st = pack_static_b(op, d, L.tc_bn))) return st;
+          } else {
+            const int64_t sub = pk_b_floats_sub(d, L.tc_bn);
+            d.Bp = op->apk_dyn[npos + li] + bo;
+            d.b_pk_sub = d.sB == 0 ? 0 : sub;
+            bo += (d.sB == 0 ? 1 : d.batch) * sub;
+            if (L.ndesc != 1) return set_err(ctx, FMMT_E_STATE, "dynamic B in a multi-descriptor launch");
+            L.pack_dst = const_cast<float*>(d.Bp);
+          }
+        } else if (d.b_pk_sub == 0 && d.sB != 0 && d.batch > 1) {
+          d.b_pk_sub = pk_b_floats_sub(d, L.tc_bn);
+        }
+      }
+    }
+  // ---- z-stage operands
+  const int64_t n12 = op->n1 * op->n2, n3 = op->n3;
+  const int64_t tiles_m = (n12 + fmmt::TC_BM - 1) / fmmt::TC_BM;
+  if (op->format != FMMT_TT4D) {
+    // dynamic G_q: A(ij, c) = G[q g_stride + ij + n12 c], K = the direction's z rank
+    ZArgs za;
+    fill_zargs(op, za, 0);
+    int64_t rzmax = 1;
+    for (int64_t p = 0; p < op->ndir; ++p) rzmax = std::max<int64_t>(rzmax, za.rank_p ? (op->format == FMMT_TUCKER3D ? rk(op, p, 2) : rk(op, p, 1)) : za.rank);
+    op->gp_stride = tiles_m * ((rzmax + fmmt::TC_BK - 1) / fmmt::TC_BK) * fmmt::TC_PACK_FLOATS;
+    dev_free(op, op->gpk);
+    if ((st = dev_alloc(op, &op->gpk, op->PB * op->gp_stride * 4, MEM_WORKSPACE, "packed G"))) return st;
+    FMMT_CUDA(ctx, cudaMemsetAsync(op->gpk, 0, op->PB * op->gp_stride * 4, ctx->stream));
+    for (int bi = 0; bi < (int)op->batches.size(); ++bi) {
+      Batch& b = op->batches[bi];
+      ZArgs a;
+      fill_zargs(op, a, bi);
+      b.zp_first = (int)op->descs.size();
+      const bool per_dir = a.rank_p != nullptr;
+      for (int q = 0; q < (per_dir ? b.nq : 1); ++q) {
+        const int64_t p = b.q0 + q;
+        const int64_t k = per_dir ? (op->format == FMMT_TUCKER3D ? rk(op, p, 2) : rk(op, p, 1)) : a.rank;
+        GemmDesc d = gdx(a.G + q * a.g_stride, nullptr, nullptr, n12, 1, k, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0,
+                         per_dir ? 1 : b.nq, a.g_stride, 0, 0);
+        d.Ap = op->gpk + q * op->gp_stride;
+        d.a_nkc = (int)((k + fmmt::TC_BK - 1) / fmmt::TC_BK);
+        d.a_pk_sub = op->gp_stride;
+        d.amax = a.amax;
+        op->descs.push_back(d);
+      }
+      b.zp_n = (int)op->descs.size() - b.zp_first;
+    }
+    // static V: B(c, kz) = V[c n3 + kz] per direction (3D formats) or shared (4D): n3 <= 32 one pack of
+    // BN = max(16, n3) columns, n3 = 64 two 32-column packs (kz = 2j + h)
+    const int bn = n3 <= 16 ? 16 : 32;
+    const int npk = n3 == 64 ? 2 : 1;
+    const int64_t ncp = op->format == FMMT_TUCKER3D || op->format == FMMT_TT3D ? op->ndir : 1;
+    std::vector<int64_t> off(ncp);
+    std::vector<fmmt::PkB> items;
+    int64_t tot = 0;
+    for (int64_t p = 0; p < ncp; ++p) {
+      const int64_t k = za.rank_p ? (op->format == FMMT_TUCKER3D ? rk(op, p, 2) : rk(op, p, 1)) : za.rank;
+      const int64_t per = ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
+      off[p] = tot;
+      for (int h = 0; h < npk; ++h) {
+        fmmt::PkB it;
+        it.B = za.V + (za.v_off ? op->off[op->format == FMMT_TUCKER3D ? 3 : 2][p] : 0) + h;
+        it.b_sk = n3;
+        it.b_sn = npk;
+        it.k = (int)k;
+        it.n = (int)(n3 / npk);
+        it.out = nullptr;
+        it.bmax = za.bmax;
+        items.push_back(it);
+        tot += per;
+      }
+    }
+    dev_free(op, op->vpk_static);
+    if ((st = dev_alloc(op, &op->vpk_static, tot * 4, MEM_DERIVED, "packed V"))) return st;
+    {
+      int64_t o = 0;
+      for (auto& it : items) {
+        it.out = op->vpk_static + o;
+        o += ((it.k + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
+      }
+    }
+    fmmt::PkB* d_items = nullptr;
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&d_items, items.size() * sizeof(fmmt::PkB), ctx->stream));
+    FMMT_CUDA(ctx, cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(fmmt::PkB), cudaMemcpyHostToDevice, ctx->stream));
+    for (size_t i0 = 0; i0 < items.size(); i0 += 65535) {
+      const unsigned ny = (unsigned)std::min<size_t>(65535, items.size() - i0);
+      if (bn == 32) fmmt::k_pk_pack_b_multi<32><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
+      else fmmt::k_pk_pack_b_multi<16><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
+      FMMT_CUDA(ctx, cudaGetLastError());
+    }
+    cudaFreeAsync(d_items, ctx->stream);
+    dev_free(op, op->d_vp_off);
+    if (ncp > 1) {
+      if ((st = dev_alloc(op, &op->d_vp_off, ncp * 8, MEM_DERIVED, "packed V offsets"))) return st;
+      FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_vp_off, off.data(), ncp * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    op->vp_stride = 0;
+  } else {
+    // TT-4D: the batch's V_q (dynamic) is packed per batch: items per (q [, parity h])
+    const int64_t r2 = rk(op, 0, 1);
+    const int bn = n3 <= 16 ? 16 : 32;
+    const int npk = n3 == 64 ? 2 : 1;
+    const int64_t per = ((r2 + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
+    op->vp_stride = npk * per;
+    dev_free(op, op->Vpk);
+    if ((st = dev_alloc(op, &op->Vpk, op->PB * op->vp_stride * 4, MEM_WORKSPACE, "packed V_q"))) return st;
+    op->vpk_floats = op->PB * op->vp_stride;
+    std::vector<fmmt::PkB> items;
+    for (int64_t q = 0; q < op->PB; ++q)
+      for (int h = 0; h < npk; ++h) {
+        fmmt::PkB it;   // V_q(c, kz) = Vw[q r2 n3 + c + r2 kz]
+        it.B = op->Vw + q * r2 * n3 + h * r2;
+        it.b_sk = 1;
+        it.b_sn = npk * r2;
+        it.k = (int)r2;
+        it.n = (int)(n3 / npk);
+        it.out = op->Vpk + q * op->vp_stride + h * per;
+        it.bmax = nullptr;
+        items.push_back(it);
+      }
+    dev_free(op, op->d_vitems);
+    if ((st = dev_alloc(op, &op->d_vitems, (int64_t)(items.size() * sizeof(fmmt::PkB)), MEM_WORKSPACE, "V_q pack items")))
+      return st;
+    FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_vitems, items.data(), items.size() * sizeof(fmmt::PkB), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+    op->nvitems = (int64_t)items.size();
+  }
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  op->packed = true;
+  return FMMT_OK;
+}
 
 static fmmt_status build_plans(fmmt_op* op) {
   free_workspace(op);
   op->descs.clear();
   op->batches.clear();
-  for (auto& b : op->bpk_static) dev_free(op, b);
-  op->bpk_static.clear();
-  dev_free(op, op->Mpk);
-  op->mpk_floats = 0;
+  for (auto& e : op->pk_cache) dev_free(op, e.second);   // static packs follow the batching (direction rows)
+  op->pk_cache.clear();
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
   if (op->PB <= 0) {
-    // batch size: the per-batch intermediates L2-resident (48 MB) ...
-    const int64_t target = 48ll << 20, pdw = std::max<int64_t>(1, per_dir_ws(op));
+    // batch size: the per-batch intermediates (raw and packed) mostly L2-resident (96 MB of the 126 MB) ...
+    const int64_t target = 96ll << 20, pdw = std::max<int64_t>(1, 2 * per_dir_ws(op));
     int64_t pb = std::max<int64_t>(1, std::min<int64_t>(op->ndir, target / pdw));
     // ... unless the 4D formats' shared slice operand (streamed from HBM once per batch, pre-split = 16 B
     // per complex) outweighs them: then batches of shared / per-direction-workspace directions, up to
@@ -711,8 +921,6 @@ static fmmt_status build_plans(fmmt_op* op) {
         ds.amax = sslot(op, 0);
         ds.bmax = sslot(op, 4);
         ds.cmax = dslot(op, bi, 0);
-        if ((st = with_packed_a(op, 0, ds))) return st;
-        if ((st = with_packed_b_static(op, ds))) return st;
         add_gemm(op, b, {ds}, "slice_tucker4d");
         if ((st = tucker_chain(op, b, bi))) return st;
         break;
@@ -729,8 +937,6 @@ static fmmt_status build_plans(fmmt_op* op) {
         dm.amax = sslot(op, 5);
         dm.bmax = sslot(op, 3);
         dm.cmax = dslot(op, bi, 0);
-        if ((st = with_packed_a(op, 5, dm))) return st;
-        if ((st = with_packed_b_static(op, dm))) return st;
         add_gemm(op, b, {dm}, "slice_htucker_M");
         GemmDesc dg = gdx(op->E, op->Mw, op->Gw, n12, r3 * nq, r34, 1, 0, NODIV, n12, r3 * nq, 1, 1, 0, NODIV, n12);
         dg.amax = sslot(op, SLOT_E);
@@ -738,21 +944,7 @@ static fmmt_status build_plans(fmmt_op* op) {
         dg.cmax = dslot(op, bi, 1);
         dg.Ap = op->E_pk;
         dg.a_nkc = (int)((r34 + fmmt::TC_BK - 1) / fmmt::TC_BK);
-        float* mpk = nullptr;
-        if (dg.Ap && op->ctx->pack_b && op->ctx->gemm_impl == 1) {
-          // M_q changes every batch: pre-split it into Mpk right before the G GEMM (sized for the largest batch)
-          const int64_t need = packb_floats(dg);
-          if (op->mpk_floats < need) {
-            dev_free(op, op->Mpk);
-            op->mpk_floats = 0;
-            if ((st = dev_alloc(op, &op->Mpk, need * 4, MEM_WORKSPACE, "pre-split M"))) return st;
-            op->mpk_floats = need;
-          }
-          mpk = op->Mpk;
-          dg.Bp = mpk;
-        }
-        add_gemm(op, b, {dg}, "slice_htucker_G");
-        b.gemms.back().pack_dst = mpk;
+        add_gemm(op, b, {dg}, "slice_htucker_G");   // (M_q is packed right before it: finalize_packs)
         break;
       }
       case FMMT_TT3D: {
@@ -767,7 +959,6 @@ static fmmt_status build_plans(fmmt_op* op) {
           dh.amax = sslot(op, 1);
           dh.bmax = sslot(op, 0);
           dh.cmax = dslot(op, bi, 0);
-          if ((st = with_packed_static(op, dh))) return st;
           ds.push_back(dh);
         }
         add_gemm(op, b, ds, "restore_tt_head");
@@ -780,8 +971,6 @@ static fmmt_status build_plans(fmmt_op* op) {
         dv.amax = sslot(op, 2);
         dv.bmax = sslot(op, 3);
         dv.cmax = dslot(op, bi, 0);
-        if ((st = with_packed_a(op, 2, dv))) return st;
-        if ((st = with_packed_b_static(op, dv))) return st;
         add_gemm(op, b, {dv}, "slice_tt4d");
         break;
       }
@@ -793,6 +982,7 @@ static fmmt_status build_plans(fmmt_op* op) {
     op->zscr_elems = 0;
   }
   if ((st = ensure_zscr(op))) return st;
+  if ((st = finalize_packs(op))) return st;
   FMMT_CUDA(op->ctx, cudaStreamSynchronize(op->ctx->stream));   // static pre-splits done
   if (!op->descs.empty()) {
     if ((st = dev_alloc(op, &op->d_descs, (int64_t)(op->descs.size() * sizeof(GemmDesc)), MEM_WORKSPACE, "descriptors")))
@@ -805,15 +995,16 @@ static fmmt_status build_plans(fmmt_op* op) {
 // ============================================================== launches
 constexpr int TC_G = 1;   // thread groups per tensor-core CTA (2 = 256 threads: measured slower)
 
+constexpr int PK_NS = 8;   // operand ring stages of the packed-operand pipeline (12 KB each at BN = 32, fp16)
+
 template <int BN>
-static fmmt_status launch_tc_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
-  using Cfg = fmmt::TcGemmCfg<BN, TC_G>;
-  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_cgemm<BN, TC_G>, Cfg::SMEM));
+static fmmt_status launch_pk_bn(fmmt_ctx* ctx, const GemmLaunch& L, const GemmDesc* d) {
+  using Cfg = fmmt::PkCfg<BN, PK_NS>;
+  FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_pk_cgemm<BN, PK_NS>, Cfg::SMEM));
   const int64_t total = (int64_t)L.tc_maxtiles * L.maxsub * L.ndesc;
-  // 2 CTAs per SM resident (smem, TMEM); each walks total / grid tiles
-  const int64_t cap = (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm;
+  const int64_t cap = (int64_t)ctx->num_sms * ctx->tc_ctas_per_sm;   // resident CTAs (TMEM, smem), each walks tiles
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, cap));
-  fmmt::k_tc_cgemm<BN, TC_G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, (int)total);
+  fmmt::k_pk_cgemm<BN, PK_NS><<<grid, fmmt::PK_THREADS, Cfg::SMEM, ctx->stream>>>(d, L.tc_maxtiles, L.maxsub, (int)total);
   return FMMT_OK;
 }
 
@@ -823,8 +1014,8 @@ static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const G
   if (L.maxsub > 65535) return set_err(ctx, FMMT_E_UNSUPPORTED, "gemm sub-batch %d too large", L.maxsub);
   fmmt_status st = FMMT_OK;
   if (impl == 1) {
-    if (L.tc_bn == 32) st = launch_tc_bn<32>(ctx, L, d_descs + L.first);
-    else st = launch_tc_bn<16>(ctx, L, d_descs + L.first);
+    if (L.tc_bn == 32) st = launch_pk_bn<32>(ctx, L, d_descs + L.first);
+    else st = launch_pk_bn<16>(ctx, L, d_descs + L.first);
   } else {
     dim3 grid((unsigned)L.maxtiles, (unsigned)L.maxsub, (unsigned)L.ndesc);
     if (L.big)
@@ -839,6 +1030,8 @@ static fmmt_status launch_gemm_group(fmmt_ctx* ctx, const GemmLaunch& L, const G
 
 static fmmt_status launch_gemm(fmmt_op* op, const GemmLaunch& L) {
   fmmt_ctx* ctx = op->ctx;
+  if (ctx->gemm_impl == 1 && !op->packed)
+    return set_err(ctx, FMMT_E_STATE, "op planned for the FFMA kernels: call fmmt_set_gemm_impl before creating it");
   ProfScope ps(ctx, L.name);
   return launch_gemm_group(ctx, L, op->d_descs, ctx->gemm_impl);
 }
@@ -911,141 +1104,71 @@ static void fill_zargs(fmmt_op* op, ZArgs& a, int bi) {
   }
 }
 
-// k_tc_pack_b of the z-stage's V_q (batch of nq directions) into op->Vpk; sets a.Vp / a.vp_stride.
-template <int BN>
-static fmmt_status pack_v_bn(fmmt_op* op, ZArgs& a, int nq) {
-  fmmt_ctx* ctx = op->ctx;
-  using Cfg = fmmt::TcGemmCfg<BN, 1>;
-  const int k = a.rank, n = (int)op->n3;
-  const int64_t nkc = (k + fmmt::TC_BK - 1) / fmmt::TC_BK, tiles_n = (n + BN - 1) / BN;
-  const int64_t per_q = tiles_n * nkc * Cfg::BP_FLOATS;
-  const int64_t need = per_q * nq;
-  if (op->vpk_floats < need)   // allocated by ensure_w (outside any graph capture) for the largest batch
-    return set_err(ctx, FMMT_E_STATE, "pre-split V workspace too small (%lld < %lld floats)",
-                   (long long)op->vpk_floats, (long long)need);
-  {
-    ProfScope ps(ctx, "pack_v");
-    const int64_t items = need / Cfg::BP_FLOATS * BN * (fmmt::TC_BK / 2);
-    const unsigned grid = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
-    fmmt::k_tc_pack_b<BN><<<grid, 256, 0, ctx->stream>>>(a.V, a.v_stride, a.v_sc, a.v_sk, k, n, nq, op->Vpk, a.bmax);
-    FMMT_CUDA(ctx, cudaGetLastError());
-  }
-  a.Vp = op->Vpk;
-  a.vp_stride = per_q;
-  return FMMT_OK;
-}
-
-static fmmt_status pack_v(fmmt_op* op, ZArgs& a, int nq) {
-  switch (op->n3) {
-    case 4: case 8: case 16: return pack_v_bn<16>(op, a, nq);
-    default: return pack_v_bn<32>(op, a, nq);
-  }
-}
-
-template <int N3, int ND>
-static fmmt_status launch_tc_z_nd(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  constexpr int BN = N3 * ND < 16 ? 16 : N3 * ND;
-  constexpr int G = 1;   // 2 = even/odd kz split over two thread groups (measured slower: 1 CTA/SM by registers)
-  using Cfg = fmmt::TcGemmCfg<BN, G>;
-  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)((nq + ND - 1) / ND);
+template <int N3, int MODE>
+static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq, float2* S) {
+  constexpr int BN = N3 == 64 ? 32 : (N3 < 16 ? 16 : N3);
+  using Cfg = fmmt::PkCfg<BN, PK_NS>;
+  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
-  if (mode == fmmt::Z_RESTORE) {
-    if constexpr (ND == 1) {
-      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G>, Cfg::SMEM));
-      fmmt::k_tc_conv_z<N3, fmmt::Z_RESTORE, 1, G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(a, nq);
-    }
+  if constexpr (N3 == 64) {
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_pk_conv_z64<MODE, PK_NS>, Cfg::SMEM));
+    fmmt::k_pk_conv_z64<MODE, PK_NS><<<grid, fmmt::PK_THREADS, Cfg::SMEM, ctx->stream>>>(a, S, nq);
   } else {
-    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND, G>, Cfg::SMEM));
-    fmmt::k_tc_conv_z<N3, fmmt::Z_LOWRANK, ND, G><<<grid, Cfg::NT, Cfg::SMEM, ctx->stream>>>(a, nq);
+    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_pk_conv_z<N3, MODE, PK_NS>, Cfg::SMEM));
+    fmmt::k_pk_conv_z<N3, MODE, PK_NS><<<grid, fmmt::PK_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
   }
   FMMT_CUDA(ctx, cudaGetLastError());
   return FMMT_OK;
 }
 
-// Directions per z tile: > 1 only when all directions share G (TT-4D's T1) and the
-// V_q of consecutive directions are contiguous ([q][kz][c]), up to 2 n3 = 64 columns.
-template <int N3>
-static fmmt_status launch_tc_z(fmmt_ctx* ctx, int mode, int nq, const ZArgs& a) {
-  const bool shareable = a.g_stride == 0 && !a.v_off && a.v_stride == (int64_t)N3 * a.v_sk && mode != fmmt::Z_RESTORE;
-  if (shareable && N3 <= 32 && ctx->z_multidir) {
-    constexpr int ND = 64 / N3 > 4 ? 4 : 64 / N3;
-    return launch_tc_z_nd<N3, ND>(ctx, mode, nq, a);
+template <int MODE>
+static fmmt_status launch_pk_z_n3(fmmt_ctx* ctx, int n3, const ZArgs& a, int nq, float2* S) {
+  switch (n3) {
+    case 4: return launch_pk_z<4, MODE>(ctx, a, nq, S);
+    case 8: return launch_pk_z<8, MODE>(ctx, a, nq, S);
+    case 16: return launch_pk_z<16, MODE>(ctx, a, nq, S);
+    case 32: return launch_pk_z<32, MODE>(ctx, a, nq, S);
+    case 64: return launch_pk_z<64, MODE>(ctx, a, nq, S);
   }
-  return launch_tc_z_nd<N3, 1>(ctx, mode, nq, a);
+  return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%d", n3);
 }
 
+// The fused z-stage of a batch (or of one direction qoff of it, nq = 1, restore hook): its dynamic
+// operand was packed by run_batch_zpack.
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0,
                             int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
-  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 == 64) {
-    // tensor-core z-stage for n3 = 64: two parity passes, even-pass partial in op->zscr
+  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE) {
+    if (!op->packed)
+      return set_err(ctx, FMMT_E_STATE, "op planned for the FFMA kernels: call fmmt_set_gemm_impl before creating it");
     ZArgs a;
     fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
     a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
     a.ncomp = ncomp;
     a.p0 = p0;
-    a.G = a.G + (int64_t)qoff * a.g_stride;
-    if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
     a.Tout = Tout;
-    if (mode != fmmt::Z_RESTORE && (!op->zscr || op->zscr_elems < (int64_t)nq * ncomp * (op->n3 / 2) * a.n12))
-      return set_err(ctx, FMMT_E_STATE, "z scratch not allocated");
-    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b) {
-      // pre-split V_q per parity pass h (columns kz = 2j + h) into Vpk[h][q]
-      using PC = fmmt::TcGemmCfg<32, 1>;
-      const int k = a.rank;
-      const int64_t per_q = ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * PC::BP_FLOATS;
-      if (op->vpk_floats < 2 * per_q * nq)
-        return set_err(ctx, FMMT_E_STATE, "pre-split V workspace too small");
-      ProfScope ps2(ctx, "pack_v");
-      const int64_t items = (int64_t)nq * ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * 32 * (fmmt::TC_BK / 2);
-      const unsigned g2 = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)ctx->num_sms * 16);
-      for (int h = 0; h < 2; ++h)
-        fmmt::k_tc_pack_b<32><<<g2, 256, 0, ctx->stream>>>(a.V + (int64_t)h * a.v_sk, a.v_stride, a.v_sc, 2 * a.v_sk, k,
-                                                            32, nq, op->Vpk + (int64_t)h * nq * per_q, a.bmax);
-      FMMT_CUDA(ctx, cudaGetLastError());
-      a.Vp = op->Vpk;
-      a.vp_stride = per_q;
-    }
-    static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
-                                   "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
-    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
-    using Cfg = fmmt::TcGemmCfg<32, 1>;
-    const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
-    if (mode == fmmt::Z_RESTORE) {
-      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z64<fmmt::Z_RESTORE>, Cfg::SMEM));
-      fmmt::k_tc_conv_z64<fmmt::Z_RESTORE><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, op->zscr, nq);
+    if (op->format == FMMT_TT4D) {
+      a.Gp = op->tbar1_pk;
+      a.gp_stride = 0;
+      a.Vp = op->Vpk + (int64_t)qoff * op->vp_stride;
+      a.vp_stride = op->vp_stride;
+      a.vp_off = nullptr;
     } else {
-      FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tc_conv_z64<fmmt::Z_LOWRANK>, Cfg::SMEM));
-      fmmt::k_tc_conv_z64<fmmt::Z_LOWRANK><<<grid, 128, Cfg::SMEM, ctx->stream>>>(a, op->zscr, nq);
+      a.Gp = op->gpk + (int64_t)qoff * op->gp_stride;
+      a.gp_stride = op->gp_stride;
+      a.Vp = op->vpk_static;
+      a.vp_off = op->d_vp_off;
+      a.vp_stride = 0;
     }
-    FMMT_CUDA(ctx, cudaGetLastError());
-    return FMMT_OK;
-  }
-  if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE && op->n3 <= 32) {
-    ZArgs a;
-    fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
-    a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
-    a.ncomp = ncomp;
-    a.p0 = p0;
-    a.G = a.G + (int64_t)qoff * a.g_stride;
-    if (!a.v_off && a.V) a.V += (int64_t)qoff * a.v_stride;
-    a.Tout = Tout;
-    // TT-4D: A (T1) is pre-split once per op; pre-split this batch's V_q too, so the z-stage streams
-    // both operands with bulk copies and no per-thread conversion (FMMT_PACKB=0 disables)
-    if (op->format == FMMT_TT4D && a.Gp && ctx->pack_b && !ctx->z_multidir) {
-      fmmt_status st = pack_v(op, a, nq);
-      if (st) return st;
-    }
+    if (!a.Gp || !a.Vp) return set_err(ctx, FMMT_E_STATE, "z-stage operands not packed");
+    if (op->n3 == 64 && mode != fmmt::Z_RESTORE &&
+        (!op->zscr || op->zscr_elems < (int64_t)nq * ncomp * (op->n3 / 2) * a.n12))
+      return set_err(ctx, FMMT_E_STATE, "z scratch not allocated");
     static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
                                    "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
-    switch (op->n3) {
-      case 4: return launch_tc_z<4>(ctx, mode, nq, a);
-      case 8: return launch_tc_z<8>(ctx, mode, nq, a);
-      case 16: return launch_tc_z<16>(ctx, mode, nq, a);
-      default: return launch_tc_z<32>(ctx, mode, nq, a);
-    }
+    if (mode == fmmt::Z_RESTORE) return launch_pk_z_n3<fmmt::Z_RESTORE>(ctx, (int)op->n3, a, nq, op->zscr);
+    return launch_pk_z_n3<fmmt::Z_LOWRANK>(ctx, (int)op->n3, a, nq, op->zscr);
   }
   ZKernel k = get_z((int)op->n3, mode);
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
@@ -1066,13 +1189,40 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
 }
 
 static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
+  const bool tc = op->ctx->gemm_impl == 1;
   for (auto& L : b.gemms) {
-    if (L.pack_dst)   // the descriptor's B was produced by the previous launch: pre-split it now
-      if (fmmt_status st = launch_pack_b(op->ctx, op->descs[L.first], L.pack_dst)) return st;
+    if (tc && L.pack_a_dyn) {   // A produced by the previous launch: pre-split it now
+      int64_t items = 1;
+      for (int i = 0; i < L.ndesc; ++i) {
+        const GemmDesc& d = op->descs[L.first + i];
+        items = std::max<int64_t>(items, (int64_t)d.batch * pk_a_floats_sub(d) / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 4);
+      }
+      if (fmmt_status st = launch_pack_a_multi(op->ctx, op->d_descs + L.first, L.ndesc, items)) return st;
+    }
+    if (tc && L.pack_dst)   // B produced by the previous launch
+      if (fmmt_status st = launch_pack_b_bn(op->ctx, op->descs[L.first], L.tc_bn, L.pack_dst)) return st;
     fmmt_status st = launch_gemm(op, L);
     if (st) return st;
   }
   return FMMT_OK;
+}
+
+// The z-stage's dynamic operand of batch b: G_q packed (3D / Tucker / H-Tucker) or V_q packed (TT-4D).
+static fmmt_status run_batch_zpack(fmmt_op* op, int bi) {
+  fmmt_ctx* ctx = op->ctx;
+  if (ctx->gemm_impl != 1 || op->format == FMMT_DENSE) return FMMT_OK;
+  const Batch& b = op->batches[bi];
+  if (op->format == FMMT_TT4D) {
+    const int npk = op->n3 == 64 ? 2 : 1;
+    const unsigned ny = (unsigned)(b.nq * npk);
+    ProfScope ps(ctx, "pack_v");
+    if (op->n3 <= 16) fmmt::k_pk_pack_b_multi<16><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
+    else fmmt::k_pk_pack_b_multi<32><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
+    FMMT_CUDA(ctx, cudaGetLastError());
+    return FMMT_OK;
+  }
+  const int64_t items = op->gp_stride / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 4 * (b.zp_n == 1 ? b.nq : 1);
+  return launch_pack_a_multi(ctx, op->d_descs + b.zp_first, b.zp_n, items);
 }
 
 // Scratch of the n3 = 64 tensor-core z-stage: one batch of half-padded lines per component.
@@ -1088,28 +1238,8 @@ static fmmt_status ensure_zscr(fmmt_op* op) {
   return st;
 }
 
-// TT-4D z-stage pre-split V_q workspace (pack_v) for the largest batch.
-static fmmt_status ensure_vpk(fmmt_op* op) {
-  fmmt_ctx* ctx = op->ctx;
-  if (op->format != FMMT_TT4D || !ctx->pack_b || op->n3 > 64) return FMMT_OK;
-  int64_t nq = 1;
-  for (const Batch& b : op->batches) nq = std::max<int64_t>(nq, b.nq);
-  const int BN = op->n3 <= 16 ? 16 : 32;
-  const int64_t nkc = (rk(op, 0, 1) + fmmt::TC_BK - 1) / fmmt::TC_BK;
-  const int64_t tiles_n = op->n3 == 64 ? 2 : (op->n3 + BN - 1) / BN;   // n3 = 64: one 32-column pack per parity pass
-  const int64_t need = nq * tiles_n * nkc * (4 * BN * 2 * fmmt::TC_BK * fmmt::TC_ESZ / 4);   // BP_FLOATS: 2 NR x 2 BK, NR = 2 BN
-  if (op->vpk_floats >= need) return FMMT_OK;
-  drop_graphs(op);
-  dev_free(op, op->Vpk);
-  op->vpk_floats = 0;
-  if (fmmt_status st = dev_alloc(op, &op->Vpk, need * 4, MEM_WORKSPACE, "pre-split V workspace")) return st;
-  op->vpk_floats = need;
-  return FMMT_OK;
-}
-
 // W (the half-padded spectra of every direction and component) sized for ncomp components.
 static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
-  if (fmmt_status st = ensure_vpk(op)) return st;
   if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
   drop_graphs(op);
   const int64_t elems = op->ndir * (op->n3 / 2) * op->n1 * op->n2;
@@ -1132,8 +1262,10 @@ static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64*
   const int planes = (int)(op->ndir * ncomp * Nz);
   if ((st = reset_dyn_slots(op))) return st;
   if ((st = launch_xy(op, true, in, op->W, planes, 1.f))) return st;
-  for (const Batch& b : op->batches) {
+  for (int bi = 0; bi < (int)op->batches.size(); ++bi) {
+    const Batch& b = op->batches[bi];
     if ((st = run_batch_prep(op, b))) return st;
+    if ((st = run_batch_zpack(op, bi))) return st;
     const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
     if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr, b.q0, ncomp))) return st;
   }
@@ -1277,9 +1409,6 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   ctx->world = world;
   if (const char* e = getenv("FMMT_GEMM")) ctx->gemm_impl = (strcmp(e, "ffma") == 0) ? 0 : 1;
   if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
-  if (const char* e = getenv("FMMT_ZMULTI")) ctx->z_multidir = atoi(e) != 0;
-  if (const char* e = getenv("FMMT_PACK")) ctx->pack_factors = atoi(e) != 0;
-  if (const char* e = getenv("FMMT_PACKB")) ctx->pack_b = atoi(e) != 0;
   if (const char* e = getenv("FMMT_AGG_STAGED")) ctx->agg_staged = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
@@ -1384,7 +1513,24 @@ fmmt_status fmmt_test_cgemm(fmmt_ctx* ctx, int impl, int64_t m, int64_t n, int64
   if (!st) st = absmax_ctx(ctx, d.B, (k - 1) * d.b_sk + (n - 1) * d.b_sn + 1, sl + 1);
   d.amax = sl;
   d.bmax = sl + 1;
+  float *apk = nullptr, *bpk = nullptr;
+  GemmDesc* dd = nullptr;
+  if (!st && impl == 1) {   // the tensor-core pipeline streams both operands pre-split
+    const int bn = n >= 32 ? 32 : 16;   // (add_gemm's choice for one descriptor)
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&apk, pk_a_floats_sub(d) * 4, ctx->stream));
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&bpk, pk_b_floats_sub(d, bn) * 4, ctx->stream));
+    d.Ap = apk;
+    d.a_nkc = (int)((k + fmmt::TC_BK - 1) / fmmt::TC_BK);
+    d.Bp = bpk;
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&dd, sizeof(GemmDesc), ctx->stream));
+    FMMT_CUDA(ctx, cudaMemcpyAsync(dd, &d, sizeof(GemmDesc), cudaMemcpyHostToDevice, ctx->stream));
+    st = launch_pack_a_multi(ctx, dd, 1, pk_a_floats_sub(d) / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 4);
+    if (!st) st = launch_pack_b_bn(ctx, d, bn, bpk);
+  }
   if (!st) st = run_one_gemm(ctx, d, impl, "test_cgemm");
+  if (dd) cudaFreeAsync(dd, ctx->stream);
+  if (apk) cudaFreeAsync(apk, ctx->stream);
+  if (bpk) cudaFreeAsync(bpk, ctx->stream);
   cudaFreeAsync(sl, ctx->stream);
   return st;
 }
@@ -1788,11 +1934,12 @@ fmmt_status fmmt_restore(fmmt_op* op, int64_t p, fmmt_c64* T_p) {
     FMMT_CUDA(ctx, cudaMemcpyAsync(T_p, op->arr[0] + p * n, n * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
     return FMMT_OK;
   }
-  if (fmmt_status st = ensure_vpk(op)) return st;
   if (fmmt_status st = reset_dyn_slots(op)) return st;
-  for (const Batch& b : op->batches) {
+  for (int bi = 0; bi < (int)op->batches.size(); ++bi) {
+    const Batch& b = op->batches[bi];
     if (p < b.q0 || p >= b.q0 + b.nq) continue;
     fmmt_status st = run_batch_prep(op, b);
+    if (!st) st = run_batch_zpack(op, bi);
     if (st) return st;
     return launch_z(op, fmmt::Z_RESTORE, (int)p, (int)(p - b.q0), 1, reinterpret_cast<float2*>(T_p));
   }
@@ -1962,7 +2109,7 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     }
     GemmDesc de = gdx(op->E, nullptr, nullptr, n12, 1, r34, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0);
     de.amax = sslot(op, SLOT_E);
-    if (ctx->pack_factors && (st = pack_a(op, de, &op->E_pk))) {
+    if ((st = pack_a(op, de, &op->E_pk))) {
       fmmt_op_destroy(op);
       return st;
     }
@@ -1988,7 +2135,7 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     }
     GemmDesc dt = gdx(op->tbar1, nullptr, nullptr, n12, 1, r2, 1, 0, NODIV, n12, 0, 0, 0, 0, NODIV, 0);
     dt.amax = sslot(op, SLOT_T1);
-    fmmt_status pst = ctx->pack_factors ? pack_a(op, dt, &op->tbar1_pk) : FMMT_OK;
+    fmmt_status pst = pack_a(op, dt, &op->tbar1_pk);
     if (pst) {
       fmmt_op_destroy(op);
       return pst;

@@ -27,9 +27,6 @@ struct fmmt_ctx {
   int num_sms = 148;                // SM count of the device (persistent grids)
   int gemm_impl = 1;                // restore GEMMs: 1 = tcgen05 3xTF32 (default), 0 = FP32 FFMA, 2 = first tcgen05 design
   bool use_graphs = true;           // replay whole matvecs as CUDA graphs (see run_graphed)
-  bool z_multidir = false;          // TT-4D z-stage: several directions per tile (1 CTA/SM; slower, A/B)
-  bool pack_b = true;               // TT-4D z-stage: pre-split V_q per batch (FMMT_PACKB=0 disables)
-  bool pack_factors = true;         // keep pre-split copies of static slice-GEMM factors (2x their bytes)
   int tc_ctas_per_sm = 2;           // tensor-core GEMM grid: CTAs per SM = the resident count (each loops over tiles)
   int tc_ctas_z = 4;                // tensor-core z-stage grid: CTAs per SM (two waves measured faster there)
   bool agg_staged = true;           // aggregation: shared-memory staged kernel (FMMT_AGG_STAGED=0: warp-per-box)

@@ -321,6 +321,8 @@ struct ZArgs {
   int z_blocked;             // tensor-core z-stage: direction-blocked tile order (shared A larger than L2 share)
   const float* amax;         // fp16-split scales: device max |G| (A) and max |V| (B); nullptr = unit scale
   const float* bmax;
+  int64_t gp_stride;         // packed G (Gp) floats per batch-local q (0 = shared G)
+  const int64_t* vp_off;     // packed V of op direction p at Vp + vp_off[p] (static per-direction factors), or nullptr
   // dense operator: T[p][k][ij]
   const float2* T;
   // restore output [k][ij]

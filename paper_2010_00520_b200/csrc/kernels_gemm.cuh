@@ -45,6 +45,10 @@ struct GemmDesc {
   const float* amax;
   const float* bmax;
   float* cmax;
+  // packed-operand strides per sub-batch (floats): A at Ap + sub * a_pk_sub, B' at Bp + sub * b_pk_sub
+  // (b_pk_sub = 0: one B shared by every sub-batch)
+  int64_t a_pk_sub;
+  int64_t b_pk_sub;
 };
 
 __device__ __forceinline__ int64_t a_row(const GemmDesc& d, int i) {
