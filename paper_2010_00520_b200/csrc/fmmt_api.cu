@@ -275,6 +275,7 @@ struct fmmt_op {
     int64_t launches = 0;   // kernels inside the graph
   };
   std::vector<GraphEntry> graphs;
+  int64_t SB = 1;                              // directions per xy sub-batch (ensure_w)
   bool translatable = true;                    // false: storage-only op (compress beyond the translate shapes)
   // fp16-split operand scales: device max(|Re|, |Im|) slots.  [0, 7) factor arrays, 7 TT-4D T1, 8 H-Tucker E
   // (set once per op); from SLOT_DYN on, 4 per batch for the intermediates its launches produce (reset to 0
@@ -849,8 +850,9 @@ static fmmt_status build_plans(fmmt_op* op) {
   op->pk_cache.clear();
   const int64_t n1 = op->n1, n2 = op->n2, n3 = op->n3, n12 = n1 * n2, Nz = n3 / 2;
   if (op->PB <= 0) {
-    // batch size: the per-batch intermediates (raw and packed) mostly L2-resident (96 MB of the 126 MB) ...
-    const int64_t target = 96ll << 20, pdw = std::max<int64_t>(1, 2 * per_dir_ws(op));
+    // batch size: the per-batch intermediates (raw and packed) within ctx->batch_mb (launch count and tail
+    // waves against L2 residency; FMMT_BATCH_MB) ...
+    const int64_t target = (int64_t)op->ctx->batch_mb << 20, pdw = std::max<int64_t>(1, 2 * per_dir_ws(op));
     int64_t pb = std::max<int64_t>(1, std::min<int64_t>(op->ndir, target / pdw));
     // ... unless the 4D formats' shared slice operand (streamed from HBM once per batch, pre-split = 16 B
     // per complex) outweighs them: then batches of shared / per-direction-workspace directions, up to
@@ -870,7 +872,7 @@ static fmmt_status build_plans(fmmt_op* op) {
   }
   const int64_t PB = op->PB;
   fmmt_status st;
-  if ((st = cmalloc(op, &op->W, op->ndir * op->w_ncomp * Nz * n12))) return st;   // all directions (one xy launch each way)
+  // (W, the half-padded spectra of one xy sub-batch, is sized by ensure_w at the first translate)
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D:
@@ -1135,7 +1137,7 @@ static fmmt_status launch_pk_z_n3(fmmt_ctx* ctx, int n3, const ZArgs& a, int nq,
 
 // The fused z-stage of a batch (or of one direction qoff of it, nq = 1, restore hook): its dynamic
 // operand was packed by run_batch_zpack.
-static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, int64_t woff = 0,
+static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, float2* Wb = nullptr,
                             int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
   if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE) {
@@ -1143,7 +1145,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
       return set_err(ctx, FMMT_E_STATE, "op planned for the FFMA kernels: call fmmt_set_gemm_impl before creating it");
     ZArgs a;
     fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
-    a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
+    a.W = Wb;
     a.ncomp = ncomp;
     a.p0 = p0;
     a.Tout = Tout;
@@ -1174,7 +1176,7 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
   ZArgs a;
   fill_zargs(op, a, (int)(p0 / std::max<int64_t>(1, op->PB)));
-  a.W = op->W + (woff + (int64_t)qoff) * ncomp * (op->n3 / 2) * a.n12;
+  a.W = Wb;
   a.ncomp = ncomp;
   a.p0 = p0;
   a.G = a.G ? a.G + (int64_t)qoff * a.g_stride : nullptr;
@@ -1195,7 +1197,7 @@ static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
       int64_t items = 1;
       for (int i = 0; i < L.ndesc; ++i) {
         const GemmDesc& d = op->descs[L.first + i];
-        items = std::max<int64_t>(items, (int64_t)d.batch * pk_a_floats_sub(d) / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 4);
+        items = std::max<int64_t>(items, (int64_t)d.batch * pk_a_floats_sub(d) / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 2);
       }
       if (fmmt_status st = launch_pack_a_multi(op->ctx, op->d_descs + L.first, L.ndesc, items)) return st;
     }
@@ -1221,14 +1223,14 @@ static fmmt_status run_batch_zpack(fmmt_op* op, int bi) {
     FMMT_CUDA(ctx, cudaGetLastError());
     return FMMT_OK;
   }
-  const int64_t items = op->gp_stride / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 4 * (b.zp_n == 1 ? b.nq : 1);
+  const int64_t items = op->gp_stride / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 2 * (b.zp_n == 1 ? b.nq : 1);
   return launch_pack_a_multi(ctx, op->d_descs + b.zp_first, b.zp_n, items);
 }
 
-// Scratch of the n3 = 64 tensor-core z-stage: one batch of half-padded lines per component.
+// Scratch of the n3 = 64 tensor-core z-stage: one sub-batch of half-padded lines per component.
 static fmmt_status ensure_zscr(fmmt_op* op) {
   if (op->n3 != 64 || op->format == FMMT_DENSE) return FMMT_OK;
-  const int64_t need = op->PB * op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2;
+  const int64_t need = std::max<int64_t>(1, op->SB) * op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2;
   if (op->zscr && op->zscr_elems >= need) return FMMT_OK;
   if (op->zscr) {
     dev_free(op, op->zscr);
@@ -1238,14 +1240,19 @@ static fmmt_status ensure_zscr(fmmt_op* op) {
   return st;
 }
 
-// W (the half-padded spectra of every direction and component) sized for ncomp components.
+// W: the half-padded spectra of one xy sub-batch (SB directions x ncomp components), sized so that the
+// forward xy FFT, the z-stage and the inverse xy FFT of a sub-batch meet in L2 (ctx->w_mb; TT-4D keeps
+// sub-batches of >= ZQB directions so its shared T1 still streams once per direction block).
 static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
   if (ncomp <= op->w_ncomp && op->W) return FMMT_OK;
   drop_graphs(op);
-  const int64_t elems = op->ndir * (op->n3 / 2) * op->n1 * op->n2;
-  dev_free(op, op->W);
   op->w_ncomp = std::max<int64_t>(ncomp, op->w_ncomp);
-  fmmt_status st = cmalloc(op, &op->W, op->w_ncomp * elems);
+  const int64_t per_dir = op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2 * 8;
+  int64_t sb = std::max<int64_t>(1, ((int64_t)op->ctx->w_mb << 20) / per_dir);
+  if (op->format == FMMT_TT4D) sb = std::max<int64_t>(sb, fmmt::ZQB);
+  op->SB = std::min<int64_t>(sb, std::max<int64_t>(1, op->PB));
+  dev_free(op, op->W);
+  fmmt_status st = cmalloc(op, &op->W, op->SB * per_dir / 8);
   if (st) return st;
   return ensure_zscr(op);
 }
@@ -1258,18 +1265,25 @@ static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64*
   // a1-a2: pruned x/y DFTs of all directions' (and components') planes in one launch (W holds
   // every half-padded spectrum, layout [p][comp][z]); per L2-sized batch: restore chain + fused
   // z-stage (one restore of T_p serves all ncomp components); a6: one launch back.
+  // per batch: the restore GEMMs; then per xy sub-batch of SB directions: forward xy FFT into W, the fused
+  // z-stage on W, inverse xy FFT out of W (W stays in L2 between the three launches)
   fmmt_status st;
-  const int planes = (int)(op->ndir * ncomp * Nz);
+  const int64_t K = (op->n1 / 2) * (op->n2 / 2) * (op->n3 / 2);
   if ((st = reset_dyn_slots(op))) return st;
-  if ((st = launch_xy(op, true, in, op->W, planes, 1.f))) return st;
+  const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
   for (int bi = 0; bi < (int)op->batches.size(); ++bi) {
     const Batch& b = op->batches[bi];
     if ((st = run_batch_prep(op, b))) return st;
     if ((st = run_batch_zpack(op, bi))) return st;
-    const int mode = op->format == FMMT_DENSE ? fmmt::Z_DENSE : fmmt::Z_LOWRANK;
-    if ((st = launch_z(op, mode, b.q0, 0, b.nq, nullptr, b.q0, ncomp))) return st;
+    for (int s0 = 0; s0 < b.nq; s0 += (int)op->SB) {
+      const int sn = (int)std::min<int64_t>(op->SB, b.nq - s0);
+      const int64_t p = b.q0 + s0;
+      const int planes = sn * ncomp * Nz;
+      if ((st = launch_xy(op, true, in + p * ncomp * K, op->W, planes, 1.f))) return st;
+      if ((st = launch_z(op, mode, (int)p, s0, sn, nullptr, op->W, ncomp))) return st;
+      if ((st = launch_xy(op, false, op->W, out + p * ncomp * K, planes, scale))) return st;
+    }
   }
-  if ((st = launch_xy(op, false, op->W, out, planes, scale))) return st;
   return FMMT_OK;
 }
 
@@ -1411,6 +1425,8 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_GRAPHS")) ctx->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("FMMT_AGG_STAGED")) ctx->agg_staged = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("FMMT_BATCH_MB")) ctx->batch_mb = std::max(1, atoi(e));
+  if (const char* e = getenv("FMMT_W_MB")) ctx->w_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {

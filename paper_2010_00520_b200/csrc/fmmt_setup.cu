@@ -425,7 +425,8 @@ struct Setup {
 static fmmt_status left_svd_from_AH(Setup& S, double2* At, int64_t rows, int64_t cols, DBuf& U, std::vector<double>& sigma) {
   fmmt_ctx* ctx = S.ctx;
   sigma.assign(rows, 0.0);
-  SETUP_TRY(dalloc(ctx, U, rows * rows * 16));
+  // U: rows x min(rows, cols) left singular vectors (economy: a tall unfolding never needs a square U)
+  SETUP_TRY(dalloc(ctx, U, rows * std::min(rows, cols) * 16));
   DBuf info, work, rwork, Sd;
   SETUP_TRY(dalloc(ctx, info, 16));
   if (cols >= rows) {
@@ -466,7 +467,7 @@ static fmmt_status left_svd_from_AH(Setup& S, double2* At, int64_t rows, int64_t
     int lw2 = 0;
     SETUP_CUSOLVER(ctx, cusolverDnZgesvd_bufferSize(S.sol, (int)rows, (int)cols, &lw2));
     SETUP_TRY(dalloc(ctx, work, (int64_t)lw2 * 16));
-    FMMT_CUDA(ctx, cudaMemsetAsync(U.p, 0, rows * rows * 16, ctx->stream));
+    FMMT_CUDA(ctx, cudaMemsetAsync(U.p, 0, rows * cols * 16, ctx->stream));
     SETUP_CUSOLVER(ctx, cusolverDnZgesvd(S.sol, 'S', 'N', (int)rows, (int)cols, A.as<zc>(), (int)rows, Sd.as<double>(), U.as<zc>(),
                                          (int)rows, nullptr, (int)cols, work.as<zc>(), lw2, rwork.as<double>(), info.as<int>()));
     std::vector<double> s(cols);
@@ -527,6 +528,73 @@ static fmmt_status mode_product(Setup& S, const double2* T, const std::vector<in
   return FMMT_OK;
 }
 
+// Left singular vectors / singular values of the mode-m unfolding of T (dims d) from its Gram matrix
+// G = T_(m) T_(m)^H (n_m x n_m; cuBLAS ZHERK over chunks of the later modes, each chunk unfolded into a
+// bounded buffer, so T is never copied whole) and its eigen-decomposition (cuSOLVER ZHEEVD):
+// sigma_i = sqrt(lambda_i) descending, U = the eigenvectors in that order.  The memory-bounded path for
+// operators too large to unfold (the paper's 256^3 x 435 sweep sizes); sigma loses relative accuracy
+// below ~1e-8 sigma_max, far beneath every truncation threshold used (gamma >= 1e-7).
+static fmmt_status gram_left_svd(Setup& S, const double2* T, const std::vector<int64_t>& d, int m, DBuf& U,
+                                 std::vector<double>& sigma) {
+  fmmt_ctx* ctx = S.ctx;
+  const int nd = (int)d.size();
+  int64_t L = 1, R = 1;
+  for (int i = 0; i < m; ++i) L *= d[i];
+  for (int i = m + 1; i < nd; ++i) R *= d[i];
+  const int64_t n = d[m];
+  const int64_t budget = 1ll << 31;   // bytes of one unfolded chunk
+  const int64_t rc = std::max<int64_t>(1, std::min<int64_t>(R, budget / std::max<int64_t>(1, L * n * 16)));
+  SETUP_TRY(dalloc(ctx, U, n * n * 16));
+  FMMT_CUDA(ctx, cudaMemsetAsync(U.p, 0, n * n * 16, ctx->stream));
+  DBuf At;
+  SETUP_TRY(dalloc(ctx, At, L * rc * n * 16));
+  const double one = 1.0;
+  for (int64_t r0 = 0; r0 < R; r0 += rc) {
+    const int64_t rn = std::min<int64_t>(rc, R - r0);
+    k_unfold_h<<<nblk(L * n * rn), 256, 0, ctx->stream>>>(T + r0 * L * n, At.as<double2>(), L, n, rn);
+    FMMT_CUDA(ctx, cudaGetLastError());
+    // G += At^H At  (At: (L rn) x n, the chunk's unfolding conjugate-transposed)
+    SETUP_CUBLAS(ctx, cublasZherk(S.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, (int)n, (int)(L * rn), &one,
+                                  (const zc*)At.as<double2>(), (int)(L * rn), &one, U.as<zc>(), (int)n));
+  }
+  DBuf W, work, info;
+  SETUP_TRY(dalloc(ctx, W, n * 8));
+  SETUP_TRY(dalloc(ctx, info, 16));
+  int lwork = 0;
+  SETUP_CUSOLVER(ctx, cusolverDnZheevd_bufferSize(S.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)n, U.as<zc>(),
+                                                   (int)n, W.as<double>(), &lwork));
+  SETUP_TRY(dalloc(ctx, work, (int64_t)lwork * 16));
+  SETUP_CUSOLVER(ctx, cusolverDnZheevd(S.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)n, U.as<zc>(), (int)n,
+                                        W.as<double>(), work.as<zc>(), lwork, info.as<int>()));
+  std::vector<double> lam(n);
+  FMMT_CUDA(ctx, cudaMemcpyAsync(lam.data(), W.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  int hinfo = 0;
+  FMMT_CUDA(ctx, cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (hinfo != 0) return set_err(ctx, FMMT_E_CUDA, "cuSOLVER zheevd info = %d", hinfo);
+  // ascending eigenpairs -> descending singular triplets: reverse the columns
+  DBuf Ur;
+  SETUP_TRY(dalloc(ctx, Ur, n * n * 16));
+  for (int64_t i = 0; i < n; ++i)
+    FMMT_CUDA(ctx, cudaMemcpyAsync(Ur.as<double2>() + i * n, U.as<double2>() + (n - 1 - i) * n, n * 16,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  std::swap(U.p, Ur.p);
+  sigma.assign(n, 0.0);
+  for (int64_t i = 0; i < n; ++i) sigma[i] = std::sqrt(std::max(0.0, lam[n - 1 - i]));
+  return FMMT_OK;
+}
+
+// Whether unfolding T (one more copy of `total` complex128) fits the device with headroom; else the Gram path.
+static bool unfold_fits(fmmt_ctx* ctx, int64_t total) {
+  if (const char* e = getenv("FMMT_COMPRESS_GRAM")) return atoi(e) == 0;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return (double)total * 16.0 * 2.5 < (double)fr;
+}
+
 // Alg. 1: classical HOSVD of T (dims d), delta = gamma / sqrt(n_trunc) * norm.
 // Returns factors U_i (n_i x r_i, device) and the projected core (device).
 struct TuckerOut {
@@ -545,21 +613,52 @@ static fmmt_status tucker_svd(Setup& S, const double2* T, const std::vector<int6
   out.U.clear();
   out.U.resize(nd);
   out.r.assign(nd, 1);
+  const bool gram = !unfold_fits(ctx, total);
   DBuf At;
-  SETUP_TRY(dalloc(ctx, At, total * 16));
+  if (!gram) SETUP_TRY(dalloc(ctx, At, total * 16));
   for (int m = 0; m < nd; ++m) {
     int64_t L = 1, R = 1;
     for (int i = 0; i < m; ++i) L *= d[i];
     for (int i = m + 1; i < nd; ++i) R *= d[i];
-    k_unfold_h<<<nblk(total), 256, 0, ctx->stream>>>(T, At.as<double2>(), L, d[m], R);
-    FMMT_CUDA(ctx, cudaGetLastError());
     std::vector<double> sigma;
     DBuf Ufull;
-    SETUP_TRY(left_svd_from_AH(S, At.as<double2>(), d[m], L * R, Ufull, sigma));
+    if (gram) {
+      SETUP_TRY(gram_left_svd(S, T, d, m, Ufull, sigma));
+    } else {
+      k_unfold_h<<<nblk(total), 256, 0, ctx->stream>>>(T, At.as<double2>(), L, d[m], R);
+      FMMT_CUDA(ctx, cudaGetLastError());
+      SETUP_TRY(left_svd_from_AH(S, At.as<double2>(), d[m], L * R, Ufull, sigma));
+    }
     const int64_t r = tail_rank(sigma, delta);
     out.r[m] = r;
     SETUP_TRY(dalloc(ctx, out.U[m], d[m] * r * 16));
     FMMT_CUDA(ctx, cudaMemcpyAsync(out.U[m].p, Ufull.p, d[m] * r * 16, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  At = DBuf();
+  if (gram && nd == 4) {
+    // core = T x_1 U1^H x_2 U2^H x_3 U3^H x_4 U4^H in chunks of the last mode (bounded temporaries):
+    // W[:, p] = (T[:, :, :, p] x_1 U1^H x_2 U2^H x_3 U3^H), then W x_4 U4^H
+    const int64_t r123 = out.r[0] * out.r[1] * out.r[2], n123 = d[0] * d[1] * d[2];
+    DBuf Wc;
+    SETUP_TRY(dalloc(ctx, Wc, r123 * d[3] * 16));
+    const int64_t pc = std::max<int64_t>(1, std::min<int64_t>(d[3], (1ll << 31) / (n123 * 16)));
+    for (int64_t p0 = 0; p0 < d[3]; p0 += pc) {
+      const int64_t pn = std::min<int64_t>(pc, d[3] - p0);
+      std::vector<int64_t> cur = {d[0], d[1], d[2], pn};
+      DBuf a, b;
+      const double2* src = T + p0 * n123;
+      for (int m = 0; m < 3; ++m) {
+        DBuf& dst = (m % 2 == 0) ? a : b;
+        SETUP_TRY(mode_product(S, src, cur, m, out.U[m].as<double2>(), out.r[m], true, dst));
+        cur[m] = out.r[m];
+        src = dst.as<double2>();
+      }
+      FMMT_CUDA(ctx, cudaMemcpyAsync(Wc.as<double2>() + p0 * r123, a.p, r123 * pn * 16, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));   // (after 3 products the result is in `a`)
+    }
+    std::vector<int64_t> cur = {out.r[0], out.r[1], out.r[2], d[3]};
+    SETUP_TRY(mode_product(S, Wc.as<double2>(), cur, 3, out.U[3].as<double2>(), out.r[3], true, out.core));
+    return FMMT_OK;
   }
   // core = T x_1 U1^H x_2 ... (step 8)
   std::vector<int64_t> cur = d;

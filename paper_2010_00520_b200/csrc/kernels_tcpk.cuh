@@ -386,60 +386,71 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_pk_conv_z64(ZArgs a, float2* 
 
 // ---------------------------------------------------------------- multi-operand packs
 // Pack the A operand of every descriptor of a list (blockIdx.y = descriptor), all sub-batches, into
-// its d.Ap (sub-batch s at d.Ap + s * d.a_pk_sub), as k_tc_pack_a; the scale from *d.amax.
+// its d.Ap (sub-batch s at d.Ap + s * d.a_pk_sub), as k_tc_pack_a; the scale from *d.amax.  One item =
+// one row and four consecutive complex K (16 B of hi, 16 B of lo in the fp16 layout: one core-matrix
+// row), threads ordered along the operand's contiguous index so loads coalesce and each warp's
+// stores cover whole 16-byte core rows.
 __global__ void k_pk_pack_a_multi(const GemmDesc* __restrict__ descs) {
   const GemmDesc& d = descs[blockIdx.y];
   const int nkc = (d.k + TC_BK - 1) / TC_BK;
   const int64_t tiles_m = (d.m + TC_BM - 1) / TC_BM;
-  const int64_t per = tiles_m * TC_BM * nkc * (TC_BK / 2);
+  constexpr int KQ = TC_BK / 4;                              // 4-complex groups per chunk
+  const int64_t per = tiles_m * TC_BM * nkc * KQ;
   const int64_t total = per * d.batch;
   const float s = (TC_F16 && d.amax) ? tc::f16_scale(*d.amax) : 1.f;
   float* out = const_cast<float*>(d.Ap);
-  // thread order: along the operand's contiguous index (rows when a_s0 == 1, else K pairs) so loads coalesce
-  const bool kfast = d.a_sk == 1 && d.a_s0 != 1;
+  const bool kfast = d.a_sk == 1 && d.a_s0 != 1;   // K contiguous in memory: K groups fastest
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t sub = e / per;
     int64_t t = e - sub * per;
-    int r, kp;
+    int r, kq;
     if (kfast) {
-      kp = (int)(t % (TC_BK / 2));
-      t /= (TC_BK / 2);
+      kq = (int)(t % KQ);
+      t /= KQ;
       r = (int)(t % TC_BM);
       t /= TC_BM;
     } else {
       r = (int)(t % TC_BM);
       t /= TC_BM;
-      kp = (int)(t % (TC_BK / 2));
-      t /= (TC_BK / 2);
+      kq = (int)(t % KQ);
+      t /= KQ;
     }
     const int kc = (int)(t % nkc);
     const int64_t tm = t / nkc;
     const int gm = (int)(tm * TC_BM + r);
-    const int gk = kc * TC_BK + 2 * kp;
+    const int gk = kc * TC_BK + 4 * kq;
     const float2* A = d.A + sub * d.sA;
-    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+    float2 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float2(0.f, 0.f);
     if (gm < d.m) {
       const int64_t row = a_row(d, gm);
-      if (gk < d.k) a0 = A[row + (int64_t)gk * d.a_sk];
-      if (gk + 1 < d.k) a1 = A[row + (int64_t)(gk + 1) * d.a_sk];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (gk + u < d.k) a[u] = A[row + (int64_t)(gk + u) * d.a_sk];
     }
     uint8_t* tile = reinterpret_cast<uint8_t*>(out + sub * d.a_pk_sub + (tm * nkc + kc) * TC_PACK_FLOATS);
     if constexpr (TC_F16) {
-      uint2 hi, lo;
-      tc::split_f16x2(a0.x * s, a0.y * s, hi.x, lo.x);
-      tc::split_f16x2(a1.x * s, a1.y * s, hi.y, lo.y);
-      const int off = r * 16 + (kp >> 1) * (TC_BM * 16) + (kp & 1) * 8;
-      *reinterpret_cast<uint2*>(tile + off) = hi;
-      *reinterpret_cast<uint2*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
+      uint4 hi, lo;
+      tc::split_f16x2(a[0].x * s, a[0].y * s, hi.x, lo.x);
+      tc::split_f16x2(a[1].x * s, a[1].y * s, hi.y, lo.y);
+      tc::split_f16x2(a[2].x * s, a[2].y * s, hi.z, lo.z);
+      tc::split_f16x2(a[3].x * s, a[3].y * s, hi.w, lo.w);
+      const int off = r * 16 + kq * (TC_BM * 16);          // 4 complex = 8 halves = one core-matrix row
+      *reinterpret_cast<uint4*>(tile + off) = hi;
+      *reinterpret_cast<uint4*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
     } else {
-      float4 hi, lo;
-      tc::split_tf32(a0.x, hi.x, lo.x);
-      tc::split_tf32(a0.y, hi.y, lo.y);
-      tc::split_tf32(a1.x, hi.z, lo.z);
-      tc::split_tf32(a1.y, hi.w, lo.w);
-      const int off = r * 16 + kp * (TC_BM * 16);
-      *reinterpret_cast<float4*>(tile + off) = hi;
-      *reinterpret_cast<float4*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {                        // tf32: 2 complex per 16-byte core row
+        float4 hi, lo;
+        tc::split_tf32(a[2 * h].x, hi.x, lo.x);
+        tc::split_tf32(a[2 * h].y, hi.y, lo.y);
+        tc::split_tf32(a[2 * h + 1].x, hi.z, lo.z);
+        tc::split_tf32(a[2 * h + 1].y, hi.w, lo.w);
+        const int off = r * 16 + (2 * kq + h) * (TC_BM * 16);
+        *reinterpret_cast<float4*>(tile + off) = hi;
+        *reinterpret_cast<float4*>(tile + TC_PACK_FLOATS * 2 + off) = lo;
+      }
     }
   }
 }
