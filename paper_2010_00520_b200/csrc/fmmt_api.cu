@@ -151,8 +151,8 @@ XYKernels make_xy() {
   k.fwd = fmmt::k_fwd_xy<NX, NY>;
   k.inv = fmmt::k_inv_xy<NX, NY>;
   k.plane_smem = G::PLANE_SMEM;
-  int lx = G::Ny * (SX::two_pass ? std::max(SX::A, SX::B) : 1);
-  int ly = NX * (SY::two_pass ? std::max(SY::A, SY::B) : 1);
+  int lx = SX::two_pass ? G::XR * std::max(SX::A, SX::B) : G::Ny;   // line items per pass (chunked four-step)
+  int ly = SY::two_pass ? G::YC * std::max(SY::A, SY::B) : NX;
   k.lines = std::max(lx, ly);
   return k;
 }

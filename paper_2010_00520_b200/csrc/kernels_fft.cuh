@@ -33,8 +33,12 @@ template <int NX, int NY> struct XYGeom {
   static constexpr int PA = NX + 1;                                  // row pitch of bufA
   static constexpr int XT = SX::two_pass ? SX::A * (SX::B + 1) : 0;  // padded x-pass-1 row pitch
   static constexpr int BUFA = Ny * PA;
-  static constexpr int BUFB_X = SX::two_pass ? Ny * XT : 0;
-  static constexpr int BUFB_Y = SY::two_pass ? NY * NX : 0;
+  // the four-step scratch holds XR rows (x pass) / YC columns (y pass) at a time, so a 128 x 128 plane needs
+  // 84 KB of shared memory (two CTAs per SM) instead of 197 KB
+  static constexpr int XR = Ny < 16 ? Ny : 16;
+  static constexpr int YC = NX < 16 ? NX : 16;
+  static constexpr int BUFB_X = SX::two_pass ? XR * XT : 0;
+  static constexpr int BUFB_Y = SY::two_pass ? NY * YC : 0;
   static constexpr int BUFB = BUFB_X > BUFB_Y ? BUFB_X : BUFB_Y;
   static constexpr int PLANE_SMEM = BUFA + BUFB;                     // complex elements per plane
 };
@@ -70,57 +74,59 @@ __device__ __forceinline__ void x_pass(float2* bufA, float2* bufB, const float2*
     }
     __syncthreads();
   } else {
-    constexpr int A = S::A, B = S::B, XT = G::XT;
-    // pass 1: item (row, n2), n2 fastest.  inputs n = B*n1 + n2.
-    {
-      const int items = nplanes * Ny * B;
-      for (int it = tid; it < items; it += blockDim.x) {
-        const int n2 = it % B;
-        const int r = it / B;
-        const int j = r / Ny, y = r % Ny;
-        const float2* row = bufA + j * G::BUFA + y * PA;
-        float2* trow = bufB + j * G::BUFB + y * XT;
-        float2 v[A];
-        if (!INV) {
+    constexpr int A = S::A, B = S::B, XT = G::XT, XR = G::XR;
+    for (int y0 = 0; y0 < Ny; y0 += XR) {   // rows in chunks of XR (the scratch holds XR rows)
+      // pass 1: item (row, n2), n2 fastest.  inputs n = B*n1 + n2.
+      {
+        const int items = nplanes * XR * B;
+        for (int it = tid; it < items; it += blockDim.x) {
+          const int n2 = it % B;
+          const int r = it / B;
+          const int j = r / XR, yl = r % XR;
+          const float2* row = bufA + j * G::BUFA + (y0 + yl) * PA;
+          float2* trow = bufB + j * G::BUFB + yl * XT;
+          float2 v[A];
+          if (!INV) {
 #pragma unroll
-          for (int n1 = 0; n1 < A / 2; ++n1) v[n1] = row[B * n1 + n2];
-          fft_reg<A, false, true>(v);
-        } else {
+            for (int n1 = 0; n1 < A / 2; ++n1) v[n1] = row[B * n1 + n2];
+            fft_reg<A, false, true>(v);
+          } else {
 #pragma unroll
-          for (int n1 = 0; n1 < A; ++n1) v[n1] = row[B * n1 + n2];
-          fft_reg<A, true, false>(v);
-        }
+            for (int n1 = 0; n1 < A; ++n1) v[n1] = row[B * n1 + n2];
+            fft_reg<A, true, false>(v);
+          }
 #pragma unroll
-        for (int k1 = 0; k1 < A; ++k1) {
-          float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NX, INV>(stw, n2 * k1));
-          trow[k1 * (B + 1) + n2] = t;
-        }
-      }
-    }
-    __syncthreads();
-    // pass 2: item (row, k1), k1 fastest.  outputs k = k1 + A*k2.
-    {
-      const int items = nplanes * Ny * A;
-      for (int it = tid; it < items; it += blockDim.x) {
-        const int k1 = it % A;
-        const int r = it / A;
-        const int j = r / Ny, y = r % Ny;
-        float2* row = bufA + j * G::BUFA + y * PA;
-        const float2* trow = bufB + j * G::BUFB + y * XT;
-        float2 v[B];
-#pragma unroll
-        for (int n2 = 0; n2 < B; ++n2) v[n2] = trow[k1 * (B + 1) + n2];
-        fft_reg<B, INV, false>(v);
-        if (!INV) {
-#pragma unroll
-          for (int k2 = 0; k2 < B; ++k2) row[k1 + A * k2] = v[k2];
-        } else {
-#pragma unroll
-          for (int k2 = 0; k2 < B / 2; ++k2) row[k1 + A * k2] = cscale(v[k2], scale);
+          for (int k1 = 0; k1 < A; ++k1) {
+            float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NX, INV>(stw, n2 * k1));
+            trow[k1 * (B + 1) + n2] = t;
+          }
         }
       }
+      __syncthreads();
+      // pass 2: item (row, k1), k1 fastest.  outputs k = k1 + A*k2.
+      {
+        const int items = nplanes * XR * A;
+        for (int it = tid; it < items; it += blockDim.x) {
+          const int k1 = it % A;
+          const int r = it / A;
+          const int j = r / XR, yl = r % XR;
+          float2* row = bufA + j * G::BUFA + (y0 + yl) * PA;
+          const float2* trow = bufB + j * G::BUFB + yl * XT;
+          float2 v[B];
+#pragma unroll
+          for (int n2 = 0; n2 < B; ++n2) v[n2] = trow[k1 * (B + 1) + n2];
+          fft_reg<B, INV, false>(v);
+          if (!INV) {
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) row[k1 + A * k2] = v[k2];
+          } else {
+#pragma unroll
+            for (int k2 = 0; k2 < B / 2; ++k2) row[k1 + A * k2] = cscale(v[k2], scale);
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -171,42 +177,45 @@ k_fwd_xy(const float2* __restrict__ sig_in, float2* __restrict__ W, int nplanes_
       for (int k = 0; k < NY; ++k) out[k * NX] = v[k];
     }
   } else {
-    constexpr int A = SY::A, B = SY::B;
-    {
-      const int items = np * B * NX;
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int x = it % NX;
-        const int r = it / NX;
-        const int n2 = r % B, j = r / B;
-        const float2* col = bufA + j * G::BUFA + x;
-        float2* tcol = bufB + j * G::BUFB + x;
-        float2 v[A];
+    constexpr int A = SY::A, B = SY::B, YC = G::YC;
+    for (int x0 = 0; x0 < NX; x0 += YC) {   // columns in chunks of YC (the scratch holds YC columns)
+      {
+        const int items = np * B * YC;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+          const int xl = it % YC;
+          const int r = it / YC;
+          const int n2 = r % B, j = r / B;
+          const float2* col = bufA + j * G::BUFA + x0 + xl;
+          float2* tcol = bufB + j * G::BUFB + xl;
+          float2 v[A];
 #pragma unroll
-        for (int n1 = 0; n1 < A / 2; ++n1) v[n1] = col[(B * n1 + n2) * PA];
-        fft_reg<A, false, true>(v);
+          for (int n1 = 0; n1 < A / 2; ++n1) v[n1] = col[(B * n1 + n2) * PA];
+          fft_reg<A, false, true>(v);
 #pragma unroll
-        for (int k1 = 0; k1 < A; ++k1) {
-          float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NY, false>(stw, n2 * k1));
-          tcol[(k1 * B + n2) * NX] = t;
+          for (int k1 = 0; k1 < A; ++k1) {
+            float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NY, false>(stw, n2 * k1));
+            tcol[(k1 * B + n2) * YC] = t;
+          }
         }
       }
-    }
-    __syncthreads();
-    {
-      const int items = np * A * NX;
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int x = it % NX;
-        const int r = it / NX;
-        const int k1 = r % A, j = r / A;
-        const float2* tcol = bufB + j * G::BUFB + x;
-        float2 v[B];
+      __syncthreads();
+      {
+        const int items = np * A * YC;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+          const int xl = it % YC;
+          const int r = it / YC;
+          const int k1 = r % A, j = r / A;
+          const float2* tcol = bufB + j * G::BUFB + xl;
+          float2 v[B];
 #pragma unroll
-        for (int n2 = 0; n2 < B; ++n2) v[n2] = tcol[(k1 * B + n2) * NX];
-        fft_reg<B, false, false>(v);
-        float2* out = dst0 + (int64_t)j * n12 + x;
+          for (int n2 = 0; n2 < B; ++n2) v[n2] = tcol[(k1 * B + n2) * YC];
+          fft_reg<B, false, false>(v);
+          float2* out = dst0 + (int64_t)j * n12 + x0 + xl;
 #pragma unroll
-        for (int k2 = 0; k2 < B; ++k2) out[(k1 + A * k2) * NX] = v[k2];
+          for (int k2 = 0; k2 < B; ++k2) out[(k1 + A * k2) * NX] = v[k2];
+        }
       }
+      __syncthreads();
     }
   }
 }
@@ -246,42 +255,45 @@ k_inv_xy(const float2* __restrict__ W, float2* __restrict__ sig_out, int nplanes
       for (int y = 0; y < Ny; ++y) col[y * PA] = v[y];
     }
   } else {
-    constexpr int A = SY::A, B = SY::B;
-    {
-      const int items = np * B * NX;
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int x = it % NX;
-        const int r = it / NX;
-        const int n2 = r % B, j = r / B;
-        const float2* in = src0 + (int64_t)j * n12 + x;
-        float2* tcol = bufB + j * G::BUFB + x;
-        float2 v[A];
+    constexpr int A = SY::A, B = SY::B, YC = G::YC;
+    for (int x0 = 0; x0 < NX; x0 += YC) {   // columns in chunks of YC
+      {
+        const int items = np * B * YC;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+          const int xl = it % YC;
+          const int r = it / YC;
+          const int n2 = r % B, j = r / B;
+          const float2* in = src0 + (int64_t)j * n12 + x0 + xl;
+          float2* tcol = bufB + j * G::BUFB + xl;
+          float2 v[A];
 #pragma unroll
-        for (int n1 = 0; n1 < A; ++n1) v[n1] = in[(B * n1 + n2) * NX];
-        fft_reg<A, true, false>(v);
+          for (int n1 = 0; n1 < A; ++n1) v[n1] = in[(B * n1 + n2) * NX];
+          fft_reg<A, true, false>(v);
 #pragma unroll
-        for (int k1 = 0; k1 < A; ++k1) {
-          float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NY, true>(stw, n2 * k1));
-          tcol[(k1 * B + n2) * NX] = t;
+          for (int k1 = 0; k1 < A; ++k1) {
+            float2 t = (k1 == 0) ? v[k1] : cmul(v[k1], tws<NY, true>(stw, n2 * k1));
+            tcol[(k1 * B + n2) * YC] = t;
+          }
         }
       }
-    }
-    __syncthreads();
-    {
-      const int items = np * A * NX;
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int x = it % NX;
-        const int r = it / NX;
-        const int k1 = r % A, j = r / A;
-        const float2* tcol = bufB + j * G::BUFB + x;
-        float2 v[B];
+      __syncthreads();
+      {
+        const int items = np * A * YC;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+          const int xl = it % YC;
+          const int r = it / YC;
+          const int k1 = r % A, j = r / A;
+          const float2* tcol = bufB + j * G::BUFB + xl;
+          float2 v[B];
 #pragma unroll
-        for (int n2 = 0; n2 < B; ++n2) v[n2] = tcol[(k1 * B + n2) * NX];
-        fft_reg<B, true, false>(v);
-        float2* col = bufA + j * G::BUFA + x;
+          for (int n2 = 0; n2 < B; ++n2) v[n2] = tcol[(k1 * B + n2) * YC];
+          fft_reg<B, true, false>(v);
+          float2* col = bufA + j * G::BUFA + x0 + xl;
 #pragma unroll
-        for (int k2 = 0; k2 < B / 2; ++k2) col[(k1 + A * k2) * PA] = v[k2];
+          for (int k2 = 0; k2 < B / 2; ++k2) col[(k1 + A * k2) * PA] = v[k2];
+        }
       }
+      __syncthreads();
     }
   }
   __syncthreads();

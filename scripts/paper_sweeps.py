@@ -113,8 +113,28 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("sweeps", nargs="*", default=["E1"])
     ap.add_argument("--max-n", type=int, default=256)
+    ap.add_argument("--min-n", type=int, default=0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "paper_sweeps.jsonl"))
+    ap.add_argument("--inproc", action="store_true", help="run in this process (default: one process per sweep "
+                    "setting, so every setting starts with a clean device)")
     args = ap.parse_args()
+    if not args.inproc:
+        import subprocess
+        units = []
+        for sw in args.sweeps:
+            if sw == "E1":
+                units += [("E1", n) for n in (32, 64, 128, 256) if args.min_n <= n <= args.max_n]
+            elif sw == "E3":
+                units += [("E3", n) for n in (256, 192, 128, 96, 64) if args.min_n <= n <= args.max_n]
+            else:
+                units.append((sw, 0))
+        rc = 0
+        for sw, n in units:
+            cmd = [sys.executable, os.path.abspath(__file__), sw, "--inproc", "--out", args.out, "--max-n",
+                   str(n if n else args.max_n), "--min-n", str(n if n else args.min_n)]
+            r = subprocess.run(cmd)
+            rc = rc or r.returncode
+        raise SystemExit(rc)
     ctx = fmmt.Context(0, torch.cuda.current_stream().cuda_stream)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     f = open(args.out, "a")
@@ -128,7 +148,7 @@ def main():
     for sw in args.sweeps:
         if sw == "E1":        # Fig. 5, Tables I, II: 8λ ... 64λ sphere, 0.5λ boxes, 5 digits, gamma 1e-6
             for nb in (16, 32, 64, 128):
-                if 2 * nb > args.max_n:
+                if not args.min_n <= 2 * nb <= args.max_n:
                     continue
                 rec, T = one_setting(ctx, "E1", nb, 0.5, 5, 1e-6)
                 rec["paper_table2"] = PAPER_T2.get(2 * nb)
@@ -147,7 +167,7 @@ def main():
         elif sw == "E3":      # Fig. 7, Table III: 32λ sphere, box 0.25λ ... 1λ, 5 digits
             for edge in (0.25, 1 / 3, 0.5, 2 / 3, 1.0):
                 nb = int(round(32 / edge))
-                if 2 * nb > args.max_n:
+                if not args.min_n <= 2 * nb <= args.max_n:
                     continue
                 rec, T = one_setting(ctx, "E3", nb, edge, 5, 1e-6)
                 if abs(edge - 0.25) < 1e-9:
