@@ -252,8 +252,6 @@ struct fmmt_op {
   float* tbar1_pk = nullptr;                   // T1 pre-split for the tensor-core z-stage (k_tc_pack_a)
   float* E_pk = nullptr;                       // E pre-split for the tensor-core G step
   int64_t w_ncomp = 1;                         // signature components W is allocated for
-  float2* zscr = nullptr;                      // n3 = 64 tensor-core z-stage: even-pass partials (batch)
-  int64_t zscr_elems = 0;
   // workspace
   int64_t PB = 0;
   int64_t sigtmp_elems = 0;
@@ -391,7 +389,6 @@ static int64_t per_dir_ws(const fmmt_op* op) {
       break;
     }
   }
-  if (op->n3 == 64 && op->format != FMMT_DENSE) e += op->w_ncomp * 32 * n12;   // zscr (n3 = 64 z-stage)
   return e * 8;
 }
 
@@ -564,7 +561,6 @@ static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
   return FMMT_OK;
 }
 
-static fmmt_status ensure_zscr(fmmt_op* op);
 static void fill_zargs(fmmt_op* op, ZArgs& a, int bi);
 
 // ---------------------------------------------------------------- packed operands (kernels_tcpk.cuh)
@@ -757,10 +753,9 @@ static fmmt_status finalize_packs(fmmt_op* op) {
       }
       b.zp_n = (int)op->descs.size() - b.zp_first;
     }
-    // static V: B(c, kz) = V[c n3 + kz] per direction (3D formats) or shared (4D): n3 <= 32 one pack of
-    // BN = max(16, n3) columns, n3 = 64 two 32-column packs (kz = 2j + h)
-    const int bn = n3 <= 16 ? 16 : 32;
-    const int npk = n3 == 64 ? 2 : 1;
+    // static V: B(c, kz) = V[c n3 + kz] per direction (3D formats) or shared (4D): one pack of
+    // BN = max(16, n3) columns; n3 = 64 with the columns ordered [kz even | kz odd] (kzperm)
+    const int bn = n3 <= 16 ? 16 : (int)n3;
     const int64_t ncp = op->format == FMMT_TUCKER3D || op->format == FMMT_TT3D ? op->ndir : 1;
     std::vector<int64_t> off(ncp);
     std::vector<fmmt::PkB> items;
@@ -769,18 +764,17 @@ static fmmt_status finalize_packs(fmmt_op* op) {
       const int64_t k = za.rank_p ? (op->format == FMMT_TUCKER3D ? rk(op, p, 2) : rk(op, p, 1)) : za.rank;
       const int64_t per = ((k + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
       off[p] = tot;
-      for (int h = 0; h < npk; ++h) {
-        fmmt::PkB it;
-        it.B = za.V + (za.v_off ? op->off[op->format == FMMT_TUCKER3D ? 3 : 2][p] : 0) + h;
-        it.b_sk = n3;
-        it.b_sn = npk;
-        it.k = (int)k;
-        it.n = (int)(n3 / npk);
-        it.out = nullptr;
-        it.bmax = za.bmax;
-        items.push_back(it);
-        tot += per;
-      }
+      fmmt::PkB it;
+      it.B = za.V + (za.v_off ? op->off[op->format == FMMT_TUCKER3D ? 3 : 2][p] : 0);
+      it.b_sk = n3;
+      it.b_sn = 1;
+      it.k = (int)k;
+      it.n = (int)n3;
+      it.out = nullptr;
+      it.bmax = za.bmax;
+      it.kzperm = n3 == 64;
+      items.push_back(it);
+      tot += per;
     }
     dev_free(op, op->vpk_static);
     if ((st = dev_alloc(op, &op->vpk_static, tot * 4, MEM_DERIVED, "packed V"))) return st;
@@ -796,7 +790,8 @@ static fmmt_status finalize_packs(fmmt_op* op) {
     FMMT_CUDA(ctx, cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(fmmt::PkB), cudaMemcpyHostToDevice, ctx->stream));
     for (size_t i0 = 0; i0 < items.size(); i0 += 65535) {
       const unsigned ny = (unsigned)std::min<size_t>(65535, items.size() - i0);
-      if (bn == 32) fmmt::k_pk_pack_b_multi<32><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
+      if (bn == 64) fmmt::k_pk_pack_b_multi<64><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
+      else if (bn == 32) fmmt::k_pk_pack_b_multi<32><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
       else fmmt::k_pk_pack_b_multi<16><<<dim3(8, ny), 256, 0, ctx->stream>>>(d_items + i0, nullptr);
       FMMT_CUDA(ctx, cudaGetLastError());
     }
@@ -810,26 +805,25 @@ static fmmt_status finalize_packs(fmmt_op* op) {
   } else {
     // TT-4D: the batch's V_q (dynamic) is packed per batch: items per (q [, parity h])
     const int64_t r2 = rk(op, 0, 1);
-    const int bn = n3 <= 16 ? 16 : 32;
-    const int npk = n3 == 64 ? 2 : 1;
+    const int bn = n3 <= 16 ? 16 : (int)n3;
     const int64_t per = ((r2 + fmmt::TC_BK - 1) / fmmt::TC_BK) * (64 * bn * fmmt::TC_ESZ / 4);
-    op->vp_stride = npk * per;
+    op->vp_stride = per;
     dev_free(op, op->Vpk);
     if ((st = dev_alloc(op, &op->Vpk, op->PB * op->vp_stride * 4, MEM_WORKSPACE, "packed V_q"))) return st;
     op->vpk_floats = op->PB * op->vp_stride;
     std::vector<fmmt::PkB> items;
-    for (int64_t q = 0; q < op->PB; ++q)
-      for (int h = 0; h < npk; ++h) {
-        fmmt::PkB it;   // V_q(c, kz) = Vw[q r2 n3 + c + r2 kz]
-        it.B = op->Vw + q * r2 * n3 + h * r2;
-        it.b_sk = 1;
-        it.b_sn = npk * r2;
-        it.k = (int)r2;
-        it.n = (int)(n3 / npk);
-        it.out = op->Vpk + q * op->vp_stride + h * per;
-        it.bmax = nullptr;
-        items.push_back(it);
-      }
+    for (int64_t q = 0; q < op->PB; ++q) {
+      fmmt::PkB it;   // V_q(c, kz) = Vw[q r2 n3 + c + r2 kz]
+      it.B = op->Vw + q * r2 * n3;
+      it.b_sk = 1;
+      it.b_sn = r2;
+      it.k = (int)r2;
+      it.n = (int)n3;
+      it.out = op->Vpk + q * op->vp_stride;
+      it.bmax = nullptr;
+      it.kzperm = n3 == 64;
+      items.push_back(it);
+    }
     dev_free(op, op->d_vitems);
     if ((st = dev_alloc(op, &op->d_vitems, (int64_t)(items.size() * sizeof(fmmt::PkB)), MEM_WORKSPACE, "V_q pack items")))
       return st;
@@ -979,11 +973,6 @@ static fmmt_status build_plans(fmmt_op* op) {
     }
     op->batches.push_back(b);
   }
-  if (op->zscr) {   // batch size may have changed
-    dev_free(op, op->zscr);
-    op->zscr_elems = 0;
-  }
-  if ((st = ensure_zscr(op))) return st;
   if ((st = finalize_packs(op))) return st;
   FMMT_CUDA(op->ctx, cudaStreamSynchronize(op->ctx->stream));   // static pre-splits done
   if (!op->descs.empty()) {
@@ -1107,15 +1096,37 @@ static void fill_zargs(fmmt_op* op, ZArgs& a, int bi) {
 }
 
 template <int N3, int MODE>
-static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq, float2* S) {
-  constexpr int BN = N3 == 64 ? 32 : (N3 < 16 ? 16 : N3);
-  using Cfg = fmmt::PkCfg<BN, PK_NS>;
-  const int64_t total = ((a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM) * (int64_t)nq;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
+static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq) {
+  const int64_t tiles_m = (a.n12 + fmmt::TC_BM - 1) / fmmt::TC_BM;
   if constexpr (N3 == 64) {
-    FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_pk_conv_z64<MODE, PK_NS>, Cfg::SMEM));
-    fmmt::k_pk_conv_z64<MODE, PK_NS><<<grid, fmmt::PK_THREADS, Cfg::SMEM, ctx->stream>>>(a, S, nq);
+    // all 64 kz per tile, one CTA per SM (PkwCfg); shared A (TT-4D T1): 2-CTA clusters, each A chunk
+    // streamed once per pair and multicast
+    constexpr int SM = fmmt::PkwCfg<fmmt::PKW_NS>::SMEM;
+    const bool cl = ctx->z_cluster && a.g_stride == 0 && a.gp_stride == 0 && nq > 1;
+    const int CL = cl ? 2 : 1;
+    const int64_t groups = tiles_m * (int64_t)((nq + CL - 1) / CL);
+    const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CL));
+    auto kfn = cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>;
+    FMMT_CUDA(ctx, set_smem_once((const void*)kfn, SM));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * ncl);
+    cfg.blockDim = dim3(fmmt::PKW_THREADS);
+    cfg.dynamicSmemBytes = SM;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cl ? 1 : 0;
+    FMMT_CUDA(ctx, cudaLaunchKernelEx(&cfg, kfn, a, nq));
+    return FMMT_OK;
   } else {
+    constexpr int BN = N3 < 16 ? 16 : N3;
+    using Cfg = fmmt::PkCfg<BN, PK_NS>;
+    const int64_t total = tiles_m * (int64_t)nq;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)ctx->num_sms * ctx->tc_ctas_z));
     FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_pk_conv_z<N3, MODE, PK_NS>, Cfg::SMEM));
     fmmt::k_pk_conv_z<N3, MODE, PK_NS><<<grid, fmmt::PK_THREADS, Cfg::SMEM, ctx->stream>>>(a, nq);
   }
@@ -1124,13 +1135,13 @@ static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq, float2* S)
 }
 
 template <int MODE>
-static fmmt_status launch_pk_z_n3(fmmt_ctx* ctx, int n3, const ZArgs& a, int nq, float2* S) {
+static fmmt_status launch_pk_z_n3(fmmt_ctx* ctx, int n3, const ZArgs& a, int nq) {
   switch (n3) {
-    case 4: return launch_pk_z<4, MODE>(ctx, a, nq, S);
-    case 8: return launch_pk_z<8, MODE>(ctx, a, nq, S);
-    case 16: return launch_pk_z<16, MODE>(ctx, a, nq, S);
-    case 32: return launch_pk_z<32, MODE>(ctx, a, nq, S);
-    case 64: return launch_pk_z<64, MODE>(ctx, a, nq, S);
+    case 4: return launch_pk_z<4, MODE>(ctx, a, nq);
+    case 8: return launch_pk_z<8, MODE>(ctx, a, nq);
+    case 16: return launch_pk_z<16, MODE>(ctx, a, nq);
+    case 32: return launch_pk_z<32, MODE>(ctx, a, nq);
+    case 64: return launch_pk_z<64, MODE>(ctx, a, nq);
   }
   return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%d", n3);
 }
@@ -1163,14 +1174,11 @@ static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, flo
       a.vp_stride = 0;
     }
     if (!a.Gp || !a.Vp) return set_err(ctx, FMMT_E_STATE, "z-stage operands not packed");
-    if (op->n3 == 64 && mode != fmmt::Z_RESTORE &&
-        (!op->zscr || op->zscr_elems < (int64_t)nq * ncomp * (op->n3 / 2) * a.n12))
-      return set_err(ctx, FMMT_E_STATE, "z scratch not allocated");
     static const char* znames[] = {"restore_conv_z_dense", "restore_conv_z_tucker3d", "restore_conv_z_tucker4d",
                                    "restore_conv_z_htucker4d", "restore_conv_z_tt3d", "restore_conv_z_tt4d"};
     ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : znames[op->format]);
-    if (mode == fmmt::Z_RESTORE) return launch_pk_z_n3<fmmt::Z_RESTORE>(ctx, (int)op->n3, a, nq, op->zscr);
-    return launch_pk_z_n3<fmmt::Z_LOWRANK>(ctx, (int)op->n3, a, nq, op->zscr);
+    if (mode == fmmt::Z_RESTORE) return launch_pk_z_n3<fmmt::Z_RESTORE>(ctx, (int)op->n3, a, nq);
+    return launch_pk_z_n3<fmmt::Z_LOWRANK>(ctx, (int)op->n3, a, nq);
   }
   ZKernel k = get_z((int)op->n3, mode);
   if (!k.fn) return set_err(ctx, FMMT_E_UNSUPPORTED, "no z kernel for n3=%lld", (long long)op->n3);
@@ -1215,29 +1223,16 @@ static fmmt_status run_batch_zpack(fmmt_op* op, int bi) {
   if (ctx->gemm_impl != 1 || op->format == FMMT_DENSE) return FMMT_OK;
   const Batch& b = op->batches[bi];
   if (op->format == FMMT_TT4D) {
-    const int npk = op->n3 == 64 ? 2 : 1;
-    const unsigned ny = (unsigned)(b.nq * npk);
+    const unsigned ny = (unsigned)b.nq;
     ProfScope ps(ctx, "pack_v");
     if (op->n3 <= 16) fmmt::k_pk_pack_b_multi<16><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
-    else fmmt::k_pk_pack_b_multi<32><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
+    else if (op->n3 == 32) fmmt::k_pk_pack_b_multi<32><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
+    else fmmt::k_pk_pack_b_multi<64><<<dim3(16, ny), 256, 0, ctx->stream>>>(op->d_vitems, dslot(op, bi, 0));
     FMMT_CUDA(ctx, cudaGetLastError());
     return FMMT_OK;
   }
   const int64_t items = op->gp_stride / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 2 * (b.zp_n == 1 ? b.nq : 1);
   return launch_pack_a_multi(ctx, op->d_descs + b.zp_first, b.zp_n, items);
-}
-
-// Scratch of the n3 = 64 tensor-core z-stage: one sub-batch of half-padded lines per component.
-static fmmt_status ensure_zscr(fmmt_op* op) {
-  if (op->n3 != 64 || op->format == FMMT_DENSE) return FMMT_OK;
-  const int64_t need = std::max<int64_t>(1, op->SB) * op->w_ncomp * (op->n3 / 2) * op->n1 * op->n2;
-  if (op->zscr && op->zscr_elems >= need) return FMMT_OK;
-  if (op->zscr) {
-    dev_free(op, op->zscr);
-  }
-  fmmt_status st = cmalloc(op, &op->zscr, need);
-  if (!st) op->zscr_elems = need;
-  return st;
 }
 
 // W: the half-padded spectra of one xy sub-batch (SB directions x ncomp components), sized so that the
@@ -1253,8 +1248,7 @@ static fmmt_status ensure_w(fmmt_op* op, int64_t ncomp) {
   op->SB = std::min<int64_t>(sb, std::max<int64_t>(1, op->PB));
   dev_free(op, op->W);
   fmmt_status st = cmalloc(op, &op->W, op->SB * per_dir / 8);
-  if (st) return st;
-  return ensure_zscr(op);
+  return st;
 }
 
 static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64* sig_out, int ncomp = 1) {
@@ -1427,6 +1421,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_TC_CTAS")) ctx->tc_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_BATCH_MB")) ctx->batch_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_W_MB")) ctx->w_mb = std::max(1, atoi(e));
+  if (const char* e = getenv("FMMT_ZCLUSTER")) ctx->z_cluster = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {

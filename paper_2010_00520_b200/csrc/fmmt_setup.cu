@@ -312,7 +312,9 @@ static fmmt_status build_operator_impl(fmmt_ctx* ctx, int64_t Nx, int64_t Ny, in
   // T = F(T~): unnormalised forward 3D DFT, batched over directions
   cufftHandle plan;
   int dims[3] = {n3, n2, n1};   // cuFFT row-major: last dim fastest
-  const int64_t maxb = std::max<int64_t>(1, std::min<int64_t>(ndir, (int64_t)(1ll << 31) / n));
+  // batches of <= 2^28 points (4 GB of complex128) so that cuFFT's work area stays small next to the
+  // operator (the 256^3 x 435 sweep operator alone is 117 GB)
+  const int64_t maxb = std::max<int64_t>(1, std::min<int64_t>(ndir, (int64_t)(1ll << 28) / n));
   if (cufftPlanMany(&plan, 3, dims, nullptr, 1, (int)n, nullptr, 1, (int)n, CUFFT_Z2Z, (int)maxb) != CUFFT_SUCCESS) {
     cudaFree(dk);
     return set_err(ctx, FMMT_E_CUDA, "cufftPlanMany failed");
@@ -534,6 +536,8 @@ static fmmt_status mode_product(Setup& S, const double2* T, const std::vector<in
 // sigma_i = sqrt(lambda_i) descending, U = the eigenvectors in that order.  The memory-bounded path for
 // operators too large to unfold (the paper's 256^3 x 435 sweep sizes); sigma loses relative accuracy
 // below ~1e-8 sigma_max, far beneath every truncation threshold used (gamma >= 1e-7).
+static fmmt_status gram_eig(Setup& S, DBuf& U, int64_t n, bool conj_vectors, std::vector<double>& sigma);
+
 static fmmt_status gram_left_svd(Setup& S, const double2* T, const std::vector<int64_t>& d, int m, DBuf& U,
                                  std::vector<double>& sigma) {
   fmmt_ctx* ctx = S.ctx;
@@ -542,13 +546,33 @@ static fmmt_status gram_left_svd(Setup& S, const double2* T, const std::vector<i
   for (int i = 0; i < m; ++i) L *= d[i];
   for (int i = m + 1; i < nd; ++i) R *= d[i];
   const int64_t n = d[m];
-  const int64_t budget = 1ll << 31;   // bytes of one unfolded chunk
-  const int64_t rc = std::max<int64_t>(1, std::min<int64_t>(R, budget / std::max<int64_t>(1, L * n * 16)));
+  const double one = 1.0;
   SETUP_TRY(dalloc(ctx, U, n * n * 16));
   FMMT_CUDA(ctx, cudaMemsetAsync(U.p, 0, n * n * 16, ctx->stream));
+  const int64_t kmax = 1ll << 30;   // ZHERK inner-dimension chunk (int32 arguments)
+  if (L == 1) {
+    // first mode: T_(1) is T itself (n x R, column-major): G = sum over column chunks of T_c T_c^H
+    for (int64_t r0 = 0; r0 < R; r0 += kmax) {
+      const int64_t rn = std::min<int64_t>(kmax, R - r0);
+      SETUP_CUBLAS(ctx, cublasZherk(S.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, (int)n, (int)rn, &one,
+                                    (const zc*)(T + r0 * n), (int)n, &one, U.as<zc>(), (int)n));
+    }
+    return gram_eig(S, U, n, false, sigma);
+  }
+  if (R == 1 && L < (1ll << 31)) {
+    // last mode: T is X = L x n (column-major) with T_(m) = X^T, so X^H X = conj(T_(m) T_(m)^H): accumulate
+    // it over row chunks of X (no copy) and conjugate the eigenvectors
+    for (int64_t l0 = 0; l0 < L; l0 += kmax) {
+      const int64_t ln = std::min<int64_t>(kmax, L - l0);
+      SETUP_CUBLAS(ctx, cublasZherk(S.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, (int)n, (int)ln, &one,
+                                    (const zc*)(T + l0), (int)L, &one, U.as<zc>(), (int)n));
+    }
+    return gram_eig(S, U, n, true, sigma);
+  }
+  const int64_t budget = 1ll << 31;   // bytes of one unfolded chunk
+  const int64_t rc = std::max<int64_t>(1, std::min<int64_t>(R, budget / std::max<int64_t>(1, L * n * 16)));
   DBuf At;
   SETUP_TRY(dalloc(ctx, At, L * rc * n * 16));
-  const double one = 1.0;
   for (int64_t r0 = 0; r0 < R; r0 += rc) {
     const int64_t rn = std::min<int64_t>(rc, R - r0);
     k_unfold_h<<<nblk(L * n * rn), 256, 0, ctx->stream>>>(T + r0 * L * n, At.as<double2>(), L, n, rn);
@@ -557,6 +581,13 @@ static fmmt_status gram_left_svd(Setup& S, const double2* T, const std::vector<i
     SETUP_CUBLAS(ctx, cublasZherk(S.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, (int)n, (int)(L * rn), &one,
                                   (const zc*)At.as<double2>(), (int)(L * rn), &one, U.as<zc>(), (int)n));
   }
+  return gram_eig(S, U, n, false, sigma);
+}
+
+// Eigen-decomposition of the Hermitian Gram matrix held (upper triangle) in U (n x n): on return U holds the
+// eigenvectors in descending eigenvalue order (conjugated if conj_vectors) and sigma_i = sqrt(lambda_i).
+static fmmt_status gram_eig(Setup& S, DBuf& U, int64_t n, bool conj_vectors, std::vector<double>& sigma) {
+  fmmt_ctx* ctx = S.ctx;
   DBuf W, work, info;
   SETUP_TRY(dalloc(ctx, W, n * 8));
   SETUP_TRY(dalloc(ctx, info, 16));
@@ -578,7 +609,12 @@ static fmmt_status gram_left_svd(Setup& S, const double2* T, const std::vector<i
   for (int64_t i = 0; i < n; ++i)
     FMMT_CUDA(ctx, cudaMemcpyAsync(Ur.as<double2>() + i * n, U.as<double2>() + (n - 1 - i) * n, n * 16,
                                    cudaMemcpyDeviceToDevice, ctx->stream));
-  std::swap(U.p, Ur.p);
+  if (conj_vectors) {
+    k_conj<<<nblk(n * n), 256, 0, ctx->stream>>>(Ur.as<double2>(), U.as<double2>(), n * n);
+    FMMT_CUDA(ctx, cudaGetLastError());
+  } else {
+    std::swap(U.p, Ur.p);
+  }
   sigma.assign(n, 0.0);
   for (int64_t i = 0; i < n; ++i) sigma[i] = std::sqrt(std::max(0.0, lam[n - 1 - i]));
   return FMMT_OK;
@@ -693,20 +729,27 @@ static fmmt_status tt_svd(Setup& S, const double2* T, const std::vector<int64_t>
   out.cores.clear();
   out.cores.resize(nd - 1);
   out.r.assign(nd - 1, 1);
-  DBuf C, At;
-  SETUP_TRY(dalloc(ctx, C, total * 16));
-  FMMT_CUDA(ctx, cudaMemcpyAsync(C.p, T, total * 16, cudaMemcpyDeviceToDevice, ctx->stream));
+  // the remainder starts as T itself (read in place, never copied); each step's left factor comes from the
+  // unfolding's SVD when a copy of it fits, else from its Gram matrix (memory-bounded, gram_left_svd)
+  DBuf C;
+  const double2* Cp = T;
   int64_t rprev = 1, cols = total;
   const zc one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
   for (int i = 0; i < nd - 1; ++i) {
     const int64_t rows = rprev * d[i];
     cols = cols / d[i];
-    // C is rows x cols (col-major).  At = C^H
-    SETUP_TRY(dalloc(ctx, At, rows * cols * 16));
-    k_unfold_h<<<nblk(rows * cols), 256, 0, ctx->stream>>>(C.as<double2>(), At.as<double2>(), 1, rows, cols);
+    // C is rows x cols (col-major)
     std::vector<double> sigma;
     DBuf Ufull;
-    SETUP_TRY(left_svd_from_AH(S, At.as<double2>(), rows, cols, Ufull, sigma));
+    if (unfold_fits(ctx, rows * cols)) {
+      DBuf At;   // At = C^H
+      SETUP_TRY(dalloc(ctx, At, rows * cols * 16));
+      k_unfold_h<<<nblk(rows * cols), 256, 0, ctx->stream>>>(Cp, At.as<double2>(), 1, rows, cols);
+      FMMT_CUDA(ctx, cudaGetLastError());
+      SETUP_TRY(left_svd_from_AH(S, At.as<double2>(), rows, cols, Ufull, sigma));
+    } else {
+      SETUP_TRY(gram_left_svd(S, Cp, {rows, cols}, 0, Ufull, sigma));
+    }
     const int64_t r = tail_rank(sigma, delta);
     out.r[i] = r;
     SETUP_TRY(dalloc(ctx, out.cores[i], rows * r * 16));
@@ -715,8 +758,9 @@ static fmmt_status tt_svd(Setup& S, const double2* T, const std::vector<int64_t>
     DBuf Cn;
     SETUP_TRY(dalloc(ctx, Cn, r * cols * 16));
     SETUP_CUBLAS(ctx, cublasZgemm(S.blas, CUBLAS_OP_C, CUBLAS_OP_N, (int)r, (int)cols, (int)rows, &one, Ufull.as<zc>(), (int)rows,
-                                  C.as<zc>(), (int)rows, &zero, Cn.as<zc>(), (int)r));
+                                  (const zc*)Cp, (int)rows, &zero, Cn.as<zc>(), (int)r));
     std::swap(C.p, Cn.p);
+    Cp = C.as<double2>();
     rprev = r;
   }
   // tail = C^T (n_d x r_{d-1})

@@ -50,20 +50,27 @@ struct PkTile {
   int nk;
 };
 
-template <int BN, int NS>
+// CL = CTAs per cluster sharing the A operand (1, or 2: each CTA streams half of every A chunk and multicasts it
+// to both; a stage is free once both CTAs' MMAs on it completed, so mma[s] counts CL commit arrivals).
+// EG = drain/epilogue warpgroups (1: warps 0-3 drain all columns; 2: warps 0-3 the first NR / 2 and warps 4-7
+// the second NR / 2 real columns of the same 128 TMEM lanes, MMA warp 8, producer warp 9).
+template <int BN, int NS, int CL = 1, int EG = 1>
 __device__ __forceinline__ uint32_t pk_setup(uint64_t* bar, uint32_t* tslot) {
   using Cfg = PkCfg<BN, NS>;
   if ((threadIdx.x >> 5) == 0) tc::tmem_alloc<Cfg::TMEM_COLS>(tslot);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < 2 * NS + 2; ++i) tc::mbar_init(&bar[i], 1);      // mma, data, gdone
+    for (int i = 0; i < NS; ++i) tc::mbar_init(&bar[i], CL);              // mma (stage free)
 #pragma unroll
-    for (int i = 2 * NS + 2; i < 2 * NS + 4; ++i) tc::mbar_init(&bar[i], 128);   // tfree
+    for (int i = NS; i < 2 * NS + 2; ++i) tc::mbar_init(&bar[i], 1);      // data, gdone
+#pragma unroll
+    for (int i = 2 * NS + 2; i < 2 * NS + 4; ++i) tc::mbar_init(&bar[i], 128 * EG);   // tfree
     tc::fence_barrier_init();
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  if constexpr (CL > 1) tc::cluster_sync();   // the peer's multicast copies / commits target these barriers
   return *tslot;
 }
 
@@ -80,10 +87,12 @@ __device__ __forceinline__ uint32_t pk_setup(uint64_t* bar, uint32_t* tslot) {
 // The MMA warp therefore runs into tile i+1 (other TMEM slot) while warps 0-3 drain and finish tile i.
 constexpr int PK_THREADS = 192;
 
-template <int BN, int NS, class TileOf, class Epi>
+template <int BN, int NS, class TileOf, class Epi, int CL = 1, int EG = 1>
 __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint8_t* sm, uint64_t* bar, uint32_t tmem) {
   using Cfg = PkCfg<BN, NS>;
   constexpr int NR = Cfg::NR;
+  constexpr int NRG = NR / EG;   // real columns drained per epilogue warpgroup
+  static_assert(NRG % 16 == 0, "drain granularity");
   constexpr uint32_t IDESC_BP = TC_F16 ? tc::idesc_f16(TC_BM, 2 * NR) : tc::idesc_tf32(TC_BM, 2 * NR);
   constexpr uint32_t IDESC_B = TC_F16 ? tc::idesc_f16(TC_BM, NR) : tc::idesc_tf32(TC_BM, NR);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
@@ -96,24 +105,34 @@ __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint
   auto GDONE = [&](int j) { return bar_u + (2 * NS + j) * 8; };
   auto TFREE = [&](int j) { return bar_u + (2 * NS + 2 + j) * 8; };
 
-  if (warp == 5) {   // ---------------------------------------------------------------- producer
+  if (warp == 4 * EG + 1) {   // ------------------------------------------------------- producer
     int64_t c = 0;
+    const uint32_t crank = CL > 1 ? tc::cluster_rank() : 0;
     for (int i = 0; i < ntiles; ++i) {
       const PkTile t = tile_of(i);
       for (int k = 0; k < t.nk; ++k, ++c) {
         const int s = (int)(c % NS);
-        if (c >= NS) tc::mbar_wait_addr(MMA(s), (uint32_t)(((c / NS) - 1) & 1));   // stage free
+        if (c >= NS) tc::mbar_wait_addr(MMA(s), (uint32_t)(((c / NS) - 1) & 1));   // stage free (all CL CTAs)
         if (lane == 0) {
           uint64_t* db = bar + NS + s;
           tc::mbar_expect_tx(db, 2 * Cfg::A_BYTES + Cfg::BP_BYTES);
           const uint32_t st = sbase + s * Cfg::STAGE;
-          tc::bulk_g2s(st, t.apk + (int64_t)k * TC_PACK_FLOATS, 2 * Cfg::A_BYTES, db);
+          const float* ach = t.apk + (int64_t)k * TC_PACK_FLOATS;
+          if constexpr (CL == 1) {
+            tc::bulk_g2s(st, ach, 2 * Cfg::A_BYTES, db);
+          } else {   // this CTA's half of the A chunk (A_hi or A_lo) to both CTAs of the pair
+            tc::bulk_g2s_mc(st + crank * Cfg::A_BYTES, ach + crank * (Cfg::A_BYTES / 4), Cfg::A_BYTES, DATA(s), 0x3);
+          }
           tc::bulk_g2s(st + 2 * Cfg::A_BYTES, t.bpk + (int64_t)k * Cfg::BP_FLOATS, Cfg::BP_BYTES, db);
         }
         __syncwarp();
       }
     }
-  } else if (warp == 4) {   // ---------------------------------------------------------- MMA issuer
+    if constexpr (CL > 1) {   // every stage's last commits (this CTA's and the peer's) have landed before exit
+      for (int64_t e = c - NS < 0 ? 0 : c - NS; e < c; ++e)
+        tc::mbar_wait_addr(MMA((int)(e % NS)), (uint32_t)((e / NS) & 1));
+    }
+  } else if (warp == 4 * EG) {   // ----------------------------------------------------- MMA issuer
     const uint64_t dAh = tc::sdesc(sbase, Cfg::LBO_A, 128), dAl = tc::sdesc(sbase + Cfg::A_BYTES, Cfg::LBO_A, 128);
     const uint64_t dBp = tc::sdesc(sbase + 2 * Cfg::A_BYTES, Cfg::LBO_B, 128);
     int64_t c = 0;
@@ -140,39 +159,43 @@ __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint
             tc::mma_tf32_el(tx, dAl + oa, dBp + ob, IDESC_B, 1);
           }
         }
-        tc::mma_commit_el(MMA(s));
+        if constexpr (CL == 1) tc::mma_commit_el(MMA(s));
+        else tc::mma_commit_mc_el(MMA(s), 0x3);            // frees the stage in both CTAs of the pair
         if (kc % TC_FC == TC_FC - 1 || kc == nk - 1) {   // group g closed
           tc::mma_commit_el(GDONE(g & 1));
           ++g;
         }
       }
     }
-  } else {   // ---------------------------------------------------------------- warps 0-3: drain + epilogue
-    const uint32_t twarp = tmem_u + ((uint32_t)(warp * 32) << 16);
-    float acc[NR];
+  } else {   // --------------------------------------------------- warps 0 .. 4 EG - 1: drain + epilogue
+    const uint32_t twarp = tmem_u + ((uint32_t)((warp & 3) * 32) << 16);
+    const int grp = warp >> 2;
+    float acc[NRG];
     int g = 0;
     for (int i = 0; i < ntiles; ++i) {
       const int nk = tile_of(i).nk;
       if (nk <= 0) continue;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) acc[j] = 0.f;
+      for (int j = 0; j < NRG; ++j) acc[j] = 0.f;
       const int ngr = (nk + TC_FC - 1) / TC_FC;
       for (int q = 0; q < ngr; ++q, ++g) {
         tc::mbar_wait_addr(GDONE(g & 1), (uint32_t)((g >> 1) & 1));
         tc::fence_after_sync();
-        tc_flush<NR, NR>(twarp + (g & 1) * 2 * NR, 0, acc);
+        tc_flush<NR, NRG>(twarp + (g & 1) * 2 * NR, grp * NRG, acc);
         tc::fence_before_sync();
         tc::mbar_arrive(&bar[2 * NS + 2 + (g & 1)]);
       }
-      epi(i, acc);
+      if constexpr (EG == 1) epi(i, acc);
+      else epi(i, acc, grp);
     }
   }
 }
 
-template <int BN, int NS>
+template <int BN, int NS, int CL = 1, int EG = 1>
 __device__ __forceinline__ void pk_teardown(uint32_t tmem) {
   tc::fence_before_sync();
   __syncthreads();
+  if constexpr (CL > 1) tc::cluster_sync();
   if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc<PkCfg<BN, NS>::TMEM_COLS>(tmem);
 }
 
@@ -307,41 +330,63 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_pk_conv_z(ZArgs a, int nq) {
 }
 
 // ---------------------------------------------------------------- k_pk_conv_z64 (n3 = 64)
-// As k_tc_conv_z64: two parity passes (kz even / odd, 32 columns each) per (direction, m-tile), walked
-// as two consecutive tiles of the same CTA; packed V of pass h at the direction's base + h * nkc *
-// BP_FLOATS (columns kz = 2j + h); the even pass's partial inverse goes to the scratch line S.
-template <int MODE, int NS>
-__global__ void __launch_bounds__(PK_THREADS, 2) k_pk_conv_z64(ZArgs a, float2* __restrict__ S, int nq) {
-  constexpr int N3 = 64, H = 32, BN = 32;
+// One tile per (direction, m-tile) with all 64 kz columns: packed V columns ordered [kz even | kz odd]
+// (k_pk_pack_b_multi kzperm), so the MMA runs at N = 256 (A_hi x [B_hi ; B_lo]) + 128 and each A chunk
+// serves twice the columns of a 32-column pass.  Two epilogue warpgroups (EG = 2) share the tile's 128
+// TMEM lanes: group h drains the parity-h half (32 complex kz = 2j + h) and runs its half of the
+// decimated z-convolution (32-point forward DFT of the W line, twiddled for h = 1, Hadamard, inverse);
+// group 1 hands its twiddled half to group 0 through shared memory and group 0 writes the sum back
+// to W.  One CTA per SM (the two 256-column TMEM slots fill TMEM).
+// CL = 2 (shared A only, launched with 2-CTA clusters): the two CTAs of a cluster take directions 2 qp and
+// 2 qp + 1 of the same m-tile, each streaming half of every A chunk and multicasting it; with an odd
+// direction count the last pair's second CTA repeats the first's direction and skips its epilogue.
+constexpr int PKW_THREADS = 320;
+constexpr int PKW_NS = 10;
+template <int NS>
+struct PkwCfg {
+  using Cfg = PkCfg<64, NS>;
+  static constexpr int X_BYTES = TC_BM * 32 * 8;   // group 1 -> group 0 hand-over (32 complex per row)
+  static constexpr int SMEM = Cfg::SMEM + X_BYTES;
+};
+
+template <int MODE, int NS, int CL = 1>
+__global__ void __launch_bounds__(PKW_THREADS, 1) k_pk_conv_z64(ZArgs a, int nq) {
+  constexpr int N3 = 64, H = 32, BN = 64;
   using Cfg = PkCfg<BN, NS>;
   extern __shared__ __align__(1024) uint8_t pksm[];
   __shared__ __align__(8) uint64_t bar[Cfg::NBAR];
   __shared__ uint32_t tslot;
-  const uint32_t tmem = pk_setup<BN, NS>(bar, &tslot);
+  float2* X = reinterpret_cast<float2*>(pksm + Cfg::SMEM);
+  const uint32_t tmem = pk_setup<BN, NS, CL, 2>(bar, &tslot);
   const int tiles_m = (int)((a.n12 + TC_BM - 1) / TC_BM);
-  const int total = tiles_m * nq;
-  const int npairs = total > (int)blockIdx.x ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int nqc = (nq + CL - 1) / CL;                    // direction groups (pairs when CL = 2)
+  const int total = tiles_m * nqc;
+  const int cid = (int)blockIdx.x / CL, ncl = (int)gridDim.x / CL, crank = (int)blockIdx.x % CL;
+  const int ntiles = total > cid ? (total - cid + ncl - 1) / ncl : 0;
   const bool shared_a = a.g_stride == 0 && a.gp_stride == 0;
   auto tile_of = [&](int i) -> PkTile {
     int q, mt;
-    z_tile(blockIdx.x + (i >> 1) * gridDim.x, tiles_m, nq, shared_a && a.z_blocked, q, mt);
+    z_tile(cid + i * ncl, tiles_m, nqc, shared_a && a.z_blocked, q, mt);
+    q = min(q * CL + crank, nq - 1);
     const int p = a.p0 + q;
     const int k = a.rank_p ? a.rank_p[p] : a.rank;
     const int nkc = (k + TC_BK - 1) / TC_BK;
     PkTile t;
     t.apk = a.Gp + (int64_t)q * a.gp_stride + (int64_t)mt * nkc * TC_PACK_FLOATS;
-    t.bpk = a.Vp + (a.vp_off ? a.vp_off[p] : (int64_t)q * a.vp_stride) + (int64_t)(i & 1) * nkc * Cfg::BP_FLOATS;
+    t.bpk = a.Vp + (a.vp_off ? a.vp_off[p] : (int64_t)q * a.vp_stride);
     t.nk = nkc;
     return t;
   };
   const float sB0 = (TC_F16 && a.bmax) ? tc::f16_scale(*a.bmax) : 1.f;
   const float sA0 = (TC_F16 && a.amax) ? tc::f16_scale(*a.amax) : 1.f;
   const float inv = 1.f / (sA0 * sB0);
-  auto epi = [&](int i, float (&acc)[Cfg::NR]) {
+  auto epi = [&](int i, float (&acc)[Cfg::NR / 2], int h) {
     int q, mt;
-    z_tile(blockIdx.x + (i >> 1) * gridDim.x, tiles_m, nq, shared_a && a.z_blocked, q, mt);
-    const int h = i & 1;
-    const int64_t ij = (int64_t)mt * TC_BM + threadIdx.x;
+    z_tile(cid + i * ncl, tiles_m, nqc, shared_a && a.z_blocked, q, mt);
+    q = q * CL + crank;
+    if (q >= nq) return;                                 // (CL = 2, odd nq: the ghost half of the last pair)
+    const int row = threadIdx.x & (TC_BM - 1);
+    const int64_t ij = (int64_t)mt * TC_BM + row;
     const bool valid = ij < a.n12;
     if constexpr (MODE == Z_RESTORE) {
       if (valid) {
@@ -351,9 +396,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_pk_conv_z64(ZArgs a, float2* 
       }
     } else {
       for (int cc = 0; cc < a.ncomp; ++cc) {
-        const int64_t line = ((int64_t)q * a.ncomp + cc) * H * a.n12 + (valid ? ij : 0);
-        float2* Wl = a.W + line;
-        float2* Sl = S + line;
+        float2* Wl = a.W + ((int64_t)q * a.ncomp + cc) * H * a.n12 + (valid ? ij : 0);
         float2 f[H];
 #pragma unroll
         for (int z = 0; z < H; ++z) f[z] = valid ? Wl[(int64_t)z * a.n12] : make_float2(0.f, 0.f);
@@ -365,23 +408,21 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_pk_conv_z64(ZArgs a, float2* 
 #pragma unroll
         for (int m = 0; m < H; ++m) f[m] = cmul2(f[m], make_float2(acc[2 * m] * inv, acc[2 * m + 1] * inv));
         fft_reg<H, true, false>(f);
-        if (valid) {
-          if (h == 0) {
+        if (h) {
 #pragma unroll
-            for (int z = 0; z < H; ++z) Sl[(int64_t)z * a.n12] = f[z];
-          } else {
-#pragma unroll
-            for (int z = 0; z < H; ++z) {
-              const float2 odd = z ? cmul(f[z], twc<N3, true>(z)) : f[z];
-              Wl[(int64_t)z * a.n12] = cadd(Sl[(int64_t)z * a.n12], odd);
-            }
-          }
+          for (int z = 0; z < H; ++z) X[z * TC_BM + row] = z ? cmul(f[z], twc<N3, true>(z)) : f[z];
         }
+        tc::named_bar_sync(1, 256);                      // the odd half is in X (and both groups read W)
+        if (!h && valid) {
+#pragma unroll
+          for (int z = 0; z < H; ++z) Wl[(int64_t)z * a.n12] = cadd(f[z], X[z * TC_BM + row]);
+        }
+        tc::named_bar_sync(1, 256);                      // X free for the next component / tile
       }
     }
   };
-  pk_run<BN, NS>(2 * npairs, tile_of, epi, pksm, bar, tmem);
-  pk_teardown<BN, NS>(tmem);
+  pk_run<BN, NS, decltype(tile_of), decltype(epi), CL, 2>(ntiles, tile_of, epi, pksm, bar, tmem);
+  pk_teardown<BN, NS, CL, 2>(tmem);
 }
 
 // ---------------------------------------------------------------- multi-operand packs
@@ -463,6 +504,7 @@ struct PkB {
   int k, n;
   float* out;
   const float* bmax;
+  int kzperm = 0;   // 1 (n = 64 z-stage V): column j holds kz = 2 (j % 32) + j / 32, i.e. [kz even | kz odd]
 };
 
 template <int BN>
@@ -485,7 +527,8 @@ __global__ void k_pk_pack_b_multi(const PkB* __restrict__ items, const float* __
     const int gn = tn * BN + j, gk = kc * TC_BK + 2 * kp;
     float2 b0 = make_float2(0.f, 0.f), b1 = make_float2(0.f, 0.f);
     if (gn < it.n) {
-      const float2* Bq = it.B + (int64_t)gn * it.b_sn;
+      const int col = it.kzperm ? 2 * (gn & 31) + (gn >> 5) : gn;
+      const float2* Bq = it.B + (int64_t)col * it.b_sn;
       if (gk < it.k) b0 = Bq[(int64_t)gk * it.b_sk];
       if (gk + 1 < it.k) b1 = Bq[(int64_t)(gk + 1) * it.b_sk];
     }

@@ -80,6 +80,8 @@ def one_setting(ctx, tag, n_box, edge, digits, gamma, formats=FORMATS, timing=Tr
         ctx.build_operator(n_box, n_box, n_box, edge, k, L, khat, T)
         ctx.sync()
     rec["build_s"] = round(time.time() - t0, 2)
+    torch.cuda.empty_cache()
+    rec["free_gb_after_build"] = round(torch.cuda.mem_get_info()[0] / 1e9, 1)
     dense_ms = None
     translatable = n[2] <= 64
     if timing and translatable:
