@@ -141,6 +141,11 @@ def kernel_flops(fmt, info, ranks, ndir):
         w["restore_mode1"] = 8 * float(np.sum(n1 * r1 * r2 * r3))
         w["restore_mode2"] = 8 * float(np.sum(n12 * r2 * r3))
         w[f"restore_conv_z_{fmt}"] = 8 * float(np.sum(n * r3))
+    if fmt == "tucker3d":
+        # fused chain (n1 % 128 == 0, n3 = 64): mode 2 first (restore_mode2x: r1 n2 r3 r2 per direction), then
+        # modes 1 and 3 in one kernel (n1 n2 r3 r1 + n r3)
+        w["restore_mode2x"] = 8 * float(np.sum(r1 * n2 * r3 * r2))
+        w["restore_conv_z_tucker3d_fused"] = 8 * float(np.sum(n12 * r3 * r1 + n * r3))
     if fmt == "tucker4d":
         w["slice_tucker4d"] = 8 * float(np.sum(rr[:, 0] * rr[:, 1] * rr[:, 2] * rr[:, 3]))
     if fmt == "tt3d":

@@ -28,9 +28,11 @@
 #include "fmmt_internal.h"
 #include "kernels_agg.cuh"
 #include "kernels_fft.cuh"
+#include "kernels_fft_big.cuh"
 #include "kernels_gemm.cuh"
 #include "kernels_tcgemm.cuh"
 #include "kernels_tcpk.cuh"
+#include "kernels_tcfuse.cuh"
 
 using fmmt::GemmDesc;
 using fmmt::ZArgs;
@@ -135,12 +137,37 @@ static cudaError_t set_smem_once(const void* fn, int bytes) {
 
 namespace {
 
+bool xy_big_enabled = true;   // FMMT_XY_BIG=0: the chunked four-step kernels for every plane size (A/B)
+
 struct XYKernels {
   void (*fwd)(const float2*, float2*, int, int) = nullptr;
   void (*inv)(const float2*, float2*, int, int, float) = nullptr;
   int plane_smem = 0;     // complex elements per plane
   int lines = 0;          // max concurrent line-items per plane (for planes-per-CTA)
+  int big_pp = 0;         // > 0: whole-plane kernels (kernels_fft_big.cuh), big_pp planes per 512-thread CTA
+  int big_smem = 0;       // their dynamic shared memory (bytes)
 };
+
+// planes per CTA of the whole-plane kernels: the most of {4, 2, 1} whose buffers fit ~210 KB (0: none fits)
+template <int NX, int NY>
+constexpr int xy_big_pp() {
+  return (NX < 64 || NY < 64 || NX > FMMT_TW_NMAX || NY > FMMT_TW_NMAX) ? 0
+         : (4 * NY * (NX + 1) + NX + NY) * 8 <= (210 << 10) ? 4
+         : (2 * NY * (NX + 1) + NX + NY) * 8 <= (210 << 10) ? 2
+         : (NY * (NX + 1) + NX + NY) * 8 <= (227 << 10) ? 1 : 0;
+}
+
+template <int NX, int NY>
+XYKernels make_xy_big(XYKernels k) {
+  constexpr int PP = xy_big_pp<NX, NY>();
+  if constexpr (PP > 0) {
+    k.fwd = fmmt::k_fwd_xy_big<NX, NY, PP>;
+    k.inv = fmmt::k_inv_xy_big<NX, NY, PP>;
+    k.big_pp = PP;
+    k.big_smem = fmmt::XYBig<NX, NY, PP>::SMEM;
+  }
+  return k;
+}
 
 template <int NX, int NY>
 XYKernels make_xy() {
@@ -154,6 +181,7 @@ XYKernels make_xy() {
   int lx = SX::two_pass ? G::XR * std::max(SX::A, SX::B) : G::Ny;   // line items per pass (chunked four-step)
   int ly = SY::two_pass ? G::YC * std::max(SY::A, SY::B) : NX;
   k.lines = std::max(lx, ly);
+  if (xy_big_enabled) k = make_xy_big<NX, NY>(k);
   return k;
 }
 
@@ -247,6 +275,13 @@ struct fmmt_op {
   std::vector<std::vector<int64_t>> off;       // per array, per direction offsets (3D formats)
   int64_t* d_voff = nullptr;                   // per direction offset of the z-stage V factor
   int* d_rank = nullptr;                       // per direction z-stage rank (3D formats)
+  // fused Tucker-3D chain (kernels_tcfuse.cuh, fmmt_ctx::z_fuse): per batch one mode-2 GEMM into H' (op->H),
+  // then k_tucker_zf per xy sub-batch
+  bool zfused = false;
+  int* d_rank3 = nullptr;                      // [ndir][3] Tucker-3D ranks
+  float* u1pk = nullptr;                       // U1 of every direction packed as an A operand (n1 rows, K = r1)
+  int64_t* d_u1p_off = nullptr;
+  int64_t h_stride = 0;                        // H' elements per batch-local direction
   float2* tbar1 = nullptr;                     // TT-4D: T1 = U1 . C1 (Fig. 4(a) step 1), n1 n2 x r2
   float2* E = nullptr;                         // H-Tucker: (C12 . C1234) x1 U1 x2 U2, n1 n2 x r34
   float* tbar1_pk = nullptr;                   // T1 pre-split for the tensor-core z-stage (k_tc_pack_a)
@@ -260,7 +295,7 @@ struct fmmt_op {
   // every device buffer the op owns (factors, derived/pre-split operands, workspaces), with its bytes and kind:
   // fmmt_op_info sums it, fmmt_op_destroy frees what is left
   std::unordered_map<const void*, std::pair<int64_t, int>> mem;
-  int64_t r2max = 1, r3max = 1, rGmax = 1;     // workspace rank bounds
+  int64_t r1max = 1, r2max = 1, r3max = 1, rGmax = 1;     // workspace rank bounds
   std::vector<GemmDesc> descs;
   GemmDesc* d_descs = nullptr;
   std::vector<Batch> batches;
@@ -377,7 +412,9 @@ static int64_t per_dir_ws(const fmmt_op* op) {
   int64_t e = 0;   // complex elements (W, the half-padded spectra, is allocated for all directions)
   switch (op->format) {
     case FMMT_DENSE: break;
-    case FMMT_TUCKER3D: e += op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
+    case FMMT_TUCKER3D:
+      e += op->zfused ? op->n2 * fmmt::zf_hj_stride(op->r1max, op->r3max) : op->n1 * op->r2max * op->r3max + n12 * op->r3max;
+      break;
     case FMMT_TUCKER4D: e += rk(op, 0, 0) * rk(op, 0, 1) * rk(op, 0, 2) + op->n1 * op->r2max * op->r3max + n12 * op->r3max; break;
     case FMMT_HTUCKER4D: e += rk(op, 0, 2) * rk(op, 0, 5) + n12 * op->r3max; break;
     case FMMT_TT3D: e += n12 * op->rGmax; break;
@@ -518,6 +555,23 @@ static fmmt_status tucker_chain(fmmt_op* op, Batch& b, int bi) {
   // G_q is [c][ij], the layout the fused z-stage reads (A(ij, c), K = r3).
   const int64_t n1 = op->n1, n2 = op->n2, n12 = n1 * n2;
   std::vector<GemmDesc> sa, sb;
+  if (op->zfused) {
+    // fused chain (kernels_tcfuse.cuh): mode 2 first, H'_q[c + r3 a + hj j] = sum_b core_q[a + r1 b + r1 r2 c] U2[j + n2 b]
+    // (hj = r1 r3 rounded up to even: 16-byte aligned blocks for the kernel's bulk copies)
+    // (rows (c, a): c = row % r3, a = row / r3); modes 1 and 3 run inside k_tucker_zf
+    for (int q = 0; q < b.nq; ++q) {
+      const int64_t p = b.q0 + q;
+      const int64_t r1 = rk(op, p, 0), r2 = rk(op, p, 1), r3 = rk(op, p, 2);
+      GemmDesc d = gdx(op->arr[0] + op->off[0][p], op->arr[2] + op->off[2][p], op->H + q * op->h_stride, r1 * r3, n2, r2,
+                       r1 * r2, 1, r3, r1, n2, 1, 1, 0, NODIV, fmmt::zf_hj_stride(r1, r3));
+      d.amax = sslot(op, 0);
+      d.bmax = sslot(op, 2);
+      d.cmax = dslot(op, bi, 0);
+      sa.push_back(d);
+    }
+    add_gemm(op, b, sa, "restore_mode2x");
+    return FMMT_OK;
+  }
   if (op->format == FMMT_TUCKER3D) {
     for (int q = 0; q < b.nq; ++q) {
       const int64_t p = b.q0 + q;
@@ -724,17 +778,51 @@ static fmmt_status finalize_packs(fmmt_op* op) {
   // ---- z-stage operands
   const int64_t n12 = op->n1 * op->n2, n3 = op->n3;
   const int64_t tiles_m = (n12 + fmmt::TC_BM - 1) / fmmt::TC_BM;
+  if (op->zfused) {
+    // U1 of every direction as k_tucker_zf's GEMM1 A operand: A(i, a) = U1_p[i + n1 a], K = r1
+    std::vector<GemmDesc> ds;
+    std::vector<int64_t> off(op->ndir);
+    int64_t tot = 0;
+    for (int64_t p = 0; p < op->ndir; ++p) {
+      const int64_t r1 = rk(op, p, 0);
+      GemmDesc d = gdx(op->arr[1] + op->off[1][p], nullptr, nullptr, op->n1, 1, r1, 1, 0, NODIV, op->n1, 0, 0, 0, 0, NODIV, 0);
+      d.amax = sslot(op, 1);
+      d.a_nkc = (int)((r1 + fmmt::TC_BK - 1) / fmmt::TC_BK);
+      off[p] = tot;
+      tot += pk_a_floats_sub(d);
+      ds.push_back(d);
+    }
+    dev_free(op, op->u1pk);
+    if ((st = dev_alloc(op, &op->u1pk, tot * 4, MEM_DERIVED, "packed U1"))) return st;
+    int64_t items = 1;
+    for (int64_t p = 0; p < op->ndir; ++p) {
+      ds[p].Ap = op->u1pk + off[p];
+      items = std::max<int64_t>(items, pk_a_floats_sub(ds[p]) / fmmt::TC_PACK_FLOATS * fmmt::TC_BM * 2);
+    }
+    GemmDesc* dd = nullptr;
+    FMMT_CUDA(ctx, cudaMallocAsync((void**)&dd, ds.size() * sizeof(GemmDesc), ctx->stream));
+    FMMT_CUDA(ctx, cudaMemcpyAsync(dd, ds.data(), ds.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice, ctx->stream));
+    for (size_t i0 = 0; i0 < ds.size() && !st; i0 += 65535)
+      st = launch_pack_a_multi(ctx, dd + i0, (int)std::min<size_t>(65535, ds.size() - i0), items);
+    cudaFreeAsync(dd, ctx->stream);
+    if (st) return st;
+    dev_free(op, op->d_u1p_off);
+    if ((st = dev_alloc(op, &op->d_u1p_off, op->ndir * 8, MEM_DERIVED, "packed U1 offsets"))) return st;
+    FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_u1p_off, off.data(), op->ndir * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
   if (op->format != FMMT_TT4D) {
-    // dynamic G_q: A(ij, c) = G[q g_stride + ij + n12 c], K = the direction's z rank
+    // dynamic G_q: A(ij, c) = G[q g_stride + ij + n12 c], K = the direction's z rank (not for the fused chain)
     ZArgs za;
     fill_zargs(op, za, 0);
     int64_t rzmax = 1;
     for (int64_t p = 0; p < op->ndir; ++p) rzmax = std::max<int64_t>(rzmax, za.rank_p ? (op->format == FMMT_TUCKER3D ? rk(op, p, 2) : rk(op, p, 1)) : za.rank);
     op->gp_stride = tiles_m * ((rzmax + fmmt::TC_BK - 1) / fmmt::TC_BK) * fmmt::TC_PACK_FLOATS;
     dev_free(op, op->gpk);
-    if ((st = dev_alloc(op, &op->gpk, op->PB * op->gp_stride * 4, MEM_WORKSPACE, "packed G"))) return st;
-    FMMT_CUDA(ctx, cudaMemsetAsync(op->gpk, 0, op->PB * op->gp_stride * 4, ctx->stream));
-    for (int bi = 0; bi < (int)op->batches.size(); ++bi) {
+    if (!op->zfused) {
+      if ((st = dev_alloc(op, &op->gpk, op->PB * op->gp_stride * 4, MEM_WORKSPACE, "packed G"))) return st;
+      FMMT_CUDA(ctx, cudaMemsetAsync(op->gpk, 0, op->PB * op->gp_stride * 4, ctx->stream));
+    }
+    for (int bi = 0; bi < (int)op->batches.size() && !op->zfused; ++bi) {
       Batch& b = op->batches[bi];
       ZArgs a;
       fill_zargs(op, a, bi);
@@ -870,6 +958,11 @@ static fmmt_status build_plans(fmmt_op* op) {
   switch (op->format) {
     case FMMT_DENSE: break;
     case FMMT_TUCKER3D:
+      if (op->zfused) {
+        op->h_stride = n2 * fmmt::zf_hj_stride(op->r1max, op->r3max);
+        if ((st = cmalloc(op, &op->H, PB * op->h_stride))) return st;
+        break;
+      }
       if ((st = cmalloc(op, &op->H, PB * n1 * op->r2max * op->r3max))) return st;
       if ((st = cmalloc(op, &op->Gw, PB * n12 * op->rGmax))) return st;
       break;
@@ -1045,7 +1138,12 @@ static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* ou
   if (!k.fwd) return set_err(ctx, FMMT_E_UNSUPPORTED, "no xy kernel for n1=%lld n2=%lld", (long long)op->n1, (long long)op->n2);
   int threads, ppc;
   xy_shape(k, &threads, &ppc);
-  const size_t smem = (size_t)(FMMT_TW_NMAX + (int64_t)ppc * k.plane_smem) * sizeof(float2);
+  size_t smem = (size_t)(FMMT_TW_NMAX + (int64_t)ppc * k.plane_smem) * sizeof(float2);
+  if (k.big_pp) {
+    threads = fmmt::XYB_THREADS;
+    ppc = k.big_pp;
+    smem = (size_t)k.big_smem;
+  }
   const unsigned grid = (unsigned)((nplanes + ppc - 1) / ppc);
   ProfScope ps(ctx, fwd ? "fft_fwd_xy" : "fft_inv_xy");
   if (fwd) {
@@ -1101,12 +1199,41 @@ static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq) {
   if constexpr (N3 == 64) {
     // all 64 kz per tile, one CTA per SM (PkwCfg); shared A (TT-4D T1): 2-CTA clusters, each A chunk
     // streamed once per pair and multicast
-    constexpr int SM = fmmt::PkwCfg<fmmt::PKW_NS>::SMEM;
+    if (MODE == fmmt::Z_LOWRANK && ctx->z_wstage) {
+      // W tiles staged through shared memory by TMA (k_pk_conv_z64w); shared A (TT-4D T1): 2-CTA clusters
+      const bool sh = a.g_stride == 0 && a.gp_stride == 0;
+      const bool clw = sh && ctx->z_cluster && nq > 1;
+      const int CLW = clw ? 2 : 1;
+      const int SMW = sh ? fmmt::PkzwCfg<fmmt::PKZW_NS_SH>::SMEM : fmmt::PkzwCfg<fmmt::PKZW_NS>::SMEM;
+      auto kw = clw ? fmmt::k_pk_conv_z64w<fmmt::PKZW_NS_SH, 2>
+                    : (sh ? fmmt::k_pk_conv_z64w<fmmt::PKZW_NS_SH, 1> : fmmt::k_pk_conv_z64w<fmmt::PKZW_NS, 1>);
+      FMMT_CUDA(ctx, set_smem_once((const void*)kw, SMW));
+      const int64_t groups = tiles_m * (int64_t)((nq + CLW - 1) / CLW);
+      const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CLW));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CLW * ncl);
+      cfg.blockDim = dim3(fmmt::PKZW_THREADS);
+      cfg.dynamicSmemBytes = SMW;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CLW;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = clw ? 1 : 0;
+      FMMT_CUDA(ctx, cudaLaunchKernelEx(&cfg, kw, a, nq));
+      return FMMT_OK;
+    }
+    // operand ring depth: PKW_NS (10) stages of 16 KB, or 12 (FMMT_ZNS=12: the deepest that fits next to X; A/B)
+    const bool deep = ctx->z_ns == 12;
+    const int SM = deep ? fmmt::PkwCfg<12>::SMEM : fmmt::PkwCfg<fmmt::PKW_NS>::SMEM;
     const bool cl = ctx->z_cluster && a.g_stride == 0 && a.gp_stride == 0 && nq > 1;
     const int CL = cl ? 2 : 1;
     const int64_t groups = tiles_m * (int64_t)((nq + CL - 1) / CL);
     const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CL));
-    auto kfn = cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>;
+    auto kfn = deep ? (cl ? fmmt::k_pk_conv_z64<MODE, 12, 2> : fmmt::k_pk_conv_z64<MODE, 12, 1>)
+                    : (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>);
     FMMT_CUDA(ctx, set_smem_once((const void*)kfn, SM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * ncl);
@@ -1151,6 +1278,44 @@ static fmmt_status launch_pk_z_n3(fmmt_ctx* ctx, int n3, const ZArgs& a, int nq)
 static fmmt_status launch_z(fmmt_op* op, int mode, int p0, int qoff, int nq, float2* Tout, float2* Wb = nullptr,
                             int ncomp = 1) {
   fmmt_ctx* ctx = op->ctx;
+  if (op->zfused && ctx->gemm_impl != 1)
+    return set_err(ctx, FMMT_E_STATE, "op planned for the fused tensor-core chain: call fmmt_set_gemm_impl before creating it");
+  if (op->zfused && mode != fmmt::Z_DENSE) {
+    if (!op->packed) return set_err(ctx, FMMT_E_STATE, "fused Tucker-3D op not packed");
+    fmmt::ZfArgs a;
+    memset(&a, 0, sizeof(a));
+    a.W = Wb;
+    a.n12 = op->n1 * op->n2;
+    a.ncomp = ncomp;
+    a.p0 = p0;
+    a.q0 = qoff;
+    a.n1 = (int)op->n1;
+    a.U1p = op->u1pk;
+    a.u1p_off = op->d_u1p_off;
+    a.H = op->H;
+    a.h_stride = op->h_stride;
+    a.Vp = op->vpk_static;
+    a.vp_off = op->d_vp_off;
+    a.rank = op->d_rank3;
+    a.u1max = sslot(op, 1);
+    a.hmax = dslot(op, (int)(p0 / std::max<int64_t>(1, op->PB)), 0);
+    a.u3max = sslot(op, 3);
+    a.Tout = Tout;
+    const int64_t tiles = (a.n12 / fmmt::TC_BM) * nq;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)ctx->num_sms));
+    ProfScope ps(ctx, mode == fmmt::Z_RESTORE ? "restore_out" : "restore_conv_z_tucker3d_fused");
+    if constexpr (fmmt::TC_F16) {
+      if (mode == fmmt::Z_RESTORE) {
+        FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tucker_zf<fmmt::Z_RESTORE>, fmmt::ZfCfg::SMEM));
+        fmmt::k_tucker_zf<fmmt::Z_RESTORE><<<grid, fmmt::ZF_THREADS, fmmt::ZfCfg::SMEM, ctx->stream>>>(a, nq);
+      } else {
+        FMMT_CUDA(ctx, set_smem_once((const void*)fmmt::k_tucker_zf<fmmt::Z_LOWRANK>, fmmt::ZfCfg::SMEM));
+        fmmt::k_tucker_zf<fmmt::Z_LOWRANK><<<grid, fmmt::ZF_THREADS, fmmt::ZfCfg::SMEM, ctx->stream>>>(a, nq);
+      }
+    }
+    FMMT_CUDA(ctx, cudaGetLastError());
+    return FMMT_OK;
+  }
   if (ctx->gemm_impl == 1 && mode != fmmt::Z_DENSE) {
     if (!op->packed)
       return set_err(ctx, FMMT_E_STATE, "op planned for the FFMA kernels: call fmmt_set_gemm_impl before creating it");
@@ -1220,7 +1385,7 @@ static fmmt_status run_batch_prep(fmmt_op* op, const Batch& b) {
 // The z-stage's dynamic operand of batch b: G_q packed (3D / Tucker / H-Tucker) or V_q packed (TT-4D).
 static fmmt_status run_batch_zpack(fmmt_op* op, int bi) {
   fmmt_ctx* ctx = op->ctx;
-  if (ctx->gemm_impl != 1 || op->format == FMMT_DENSE) return FMMT_OK;
+  if (ctx->gemm_impl != 1 || op->format == FMMT_DENSE || op->zfused) return FMMT_OK;
   const Batch& b = op->batches[bi];
   if (op->format == FMMT_TT4D) {
     const unsigned ny = (unsigned)b.nq;
@@ -1422,6 +1587,10 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_BATCH_MB")) ctx->batch_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_W_MB")) ctx->w_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_ZCLUSTER")) ctx->z_cluster = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_XY_BIG")) xy_big_enabled = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_ZWSTAGE")) ctx->z_wstage = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_ZFUSE")) ctx->z_fuse = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_ZNS")) ctx->z_ns = atoi(e);
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {
@@ -1975,7 +2144,7 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
                       n2 <= 256 && n3 <= 64;
   if (translatable) {   // the xy FFT kernel holds one padded plane (plus twiddles) in shared memory
     const XYKernels xk = get_xy((int)n1, (int)n2);
-    translatable = xk.fwd && (int64_t)(FMMT_TW_NMAX + xk.plane_smem) * 8 <= 227 * 1024;
+    translatable = xk.fwd && (xk.big_pp > 0 || (int64_t)(FMMT_TW_NMAX + xk.plane_smem) * 8 <= 227 * 1024);
   }
   if (!translatable && !storage_only_ok)
     return set_err(ctx, FMMT_E_UNSUPPORTED,
@@ -2018,10 +2187,15 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
         if (r1 > n1 || r2 > n2 || r3 > n3) { delete op; return set_err(ctx, FMMT_E_SHAPE, "rank exceeds mode size"); }
         const int64_t sz[4] = {r1 * r2 * r3, n1 * r1, n2 * r2, n3 * r3};
         for (int i = 0; i < 4; ++i) { op->off[i][p] = elems[i]; elems[i] += sz[i]; }
+        op->r1max = std::max(op->r1max, r1);
         op->r2max = std::max(op->r2max, r2);
         op->r3max = std::max(op->r3max, r3);
       }
       op->rGmax = op->r3max;
+      // fused mode-1 / mode-3 chain (kernels_tcfuse.cuh): tensor-core fp16 build, n3 = 64, whole 128-line i-blocks,
+      // H'_j within the shared-memory region, G within 64 TMEM columns
+      op->zfused = ctx->z_fuse && ctx->gemm_impl == 1 && fmmt::TC_F16 && n3 == 64 && n1 % 128 == 0 &&
+                   op->r1max <= fmmt::ZfCfg::MAX_R1 && op->r3max <= 64;
       break;
     }
     case FMMT_TUCKER4D: {
@@ -2087,6 +2261,20 @@ fmmt_status create_op(fmmt_ctx* ctx, fmmt_format format, int64_t n1, int64_t n2,
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       fmmt_op_destroy(op);
       return set_err(ctx, FMMT_E_CUDA, "z-stage table copy failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    }
+    if (op->zfused) {
+      std::vector<int> r3t(ndir * 3);
+      for (int64_t p = 0; p < ndir; ++p)
+        for (int s3 = 0; s3 < 3; ++s3) r3t[p * 3 + s3] = (int)R(p, s3);
+      if ((st = dev_alloc(op, &op->d_rank3, ndir * 12, MEM_DERIVED, "Tucker-3D ranks"))) {
+        fmmt_op_destroy(op);
+        return st;
+      }
+      cudaError_t e3 = cudaMemcpy(op->d_rank3, r3t.data(), ndir * 12, cudaMemcpyHostToDevice);
+      if (e3 != cudaSuccess) {
+        fmmt_op_destroy(op);
+        return set_err(ctx, FMMT_E_CUDA, "rank table copy failed: %s", cudaGetErrorString(e3));
+      }
     }
   }
   if (!translatable) {   // storage-only: factors, ranks, info and export (no plans, no derived operands)

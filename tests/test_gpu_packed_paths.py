@@ -16,7 +16,7 @@ import pytest
 from oracle import fmm, translate
 from synth import signatures
 
-from tests._helpers import Compressed, operator, rel
+from tests._helpers import Compressed, operator, rel, t_lib_to_math
 
 pytestmark = pytest.mark.gpu
 
@@ -49,14 +49,14 @@ def _ctx(fm, packb: bool):
 _OPS = {}
 
 
-def _n64_operator(fmt, tol, nd=20):
-    """A small n3 = 64 grid (4 x 4 x 32 boxes, edge 0.5, L = 12): the z-stage takes the two-pass path."""
-    key = (fmt, tol, nd)
+def _n64_operator(fmt, tol, nd=20, nxy=4):
+    """A small n3 = 64 grid (nxy x nxy x 32 boxes, edge 0.5, L = 12): the z-stage takes the two-pass path."""
+    key = (fmt, tol, nd, nxy)
     if key not in _OPS:
         k = 2 * math.pi
         khat, w, _, _ = fmm.direction_grid(12, 26)
         khat, w = khat[:nd], w[:nd]
-        grid = fmm.OperatorGrid(4, 4, 32, 0.5, k, 12)
+        grid = fmm.OperatorGrid(nxy, nxy, 32, 0.5, k, 12)
         _OPS[key] = (Compressed(fmt, fmm.fft_operator_4d(grid, khat), tol), w)
     return _OPS[key]
 
@@ -120,3 +120,69 @@ def test_several_batches_match_oracle(fm, fmt):
             assert rel(cp.translate(sm, p), om[p]) <= TOL, p
     op.close()
     ctx.close()
+
+
+def _ctx_env(fm, **env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return fm.Context(0, torch.cuda.current_stream().cuda_stream)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("nxy", [4, 8])
+@pytest.mark.parametrize("ncomp", [1, 3])
+@pytest.mark.parametrize("fmt", ["tucker3d", "tt3d", "tucker4d", "htucker4d"])
+def test_n3_64_staged_w_matches_oracle(fm, fmt, ncomp, nxy):
+    """n3 = 64 z-stage with a per-direction A (k_pk_conv_z64w: W tiles staged through shared memory by the
+    TMA engine, loader warp + bulk stores): a partial m-tile (8 x 8 lines, nxy = 4) and two full m-tiles
+    (16 x 16, nxy = 8), one and three signature components; the unstaged kernel (FMMT_ZWSTAGE=0) agrees."""
+    cp, _ = _n64_operator(fmt, 1e-4, nd=12, nxy=nxy)
+    N = (nxy, nxy, 32)
+    outs = []
+    for ws in (1, 0):
+        ctx = _ctx_env(fm, FMMT_ZWSTAGE=ws)
+        outs.append(_check_multi(ctx, cp, N, ncomp, 300 + ncomp + nxy))
+        ctx.close()
+    assert rel(outs[0], outs[1]) <= 1e-6
+
+
+def _fused_operator(nx, nd=10):
+    """Tucker-3D of a grid with n1 = 2 nx >= 128 and n3 = 64 (nx x 2 x 32 boxes): the fused mode-1 / mode-3
+    z-stage (kernels_tcfuse.cuh) takes it."""
+    key = ("fused", nx, nd)
+    if key not in _OPS:
+        khat, w, _, _ = fmm.direction_grid(12, 26)
+        grid = fmm.OperatorGrid(nx, 2, 32, 0.5, 2 * math.pi, 12)
+        _OPS[key] = (Compressed("tucker3d", fmm.fft_operator_4d(grid, khat[:nd]), 1e-4), w[:nd])
+    return _OPS[key]
+
+
+@pytest.mark.parametrize("nx", [64, 128])
+@pytest.mark.parametrize("ncomp", [1, 2])
+def test_tucker3d_fused_chain_matches_oracle(fm, nx, ncomp):
+    """Fused Tucker-3D chain (restore_mode2x + k_tucker_zf: G in TMEM / shared memory only) with one and two
+    i-blocks per y index (n1 = 128, 256), one and two components: translate vs the oracle, restore vs the
+    oracle's restoration, and the unfused chain (FMMT_ZFUSE=0) agrees."""
+    cp, _ = _fused_operator(nx)
+    N = (nx, 2, 32)
+    outs = []
+    for fz in (1, 0):
+        ctx = _ctx_env(fm, FMMT_ZFUSE=fz)
+        outs.append(_check_multi(ctx, cp, N, ncomp, 400 + ncomp + nx))
+        if fz:
+            op = ctx.import_op("tucker3d", cp.n, cp.ndir, cp.ranks, cp.arrays)
+            out = torch.empty(int(np.prod(cp.n)), dtype=torch.complex64, device="cuda")
+            for p in (0, cp.ndir - 1):
+                op.restore(p, out)
+                ctx.sync()
+                got = t_lib_to_math(out.cpu().numpy(), cp.n)
+                assert rel(cp.restore(p), got) <= 1e-6, p
+            op.close()
+        ctx.close()
+    assert rel(outs[0], outs[1]) <= 1e-6

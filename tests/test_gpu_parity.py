@@ -133,11 +133,14 @@ def test_translate_parity_config3_elongated(fm, ctx, fmt, tol):
     assert max(errs) <= TRANSLATE_TOL, max(errs)
 
 
-@pytest.mark.parametrize("N", [(2, 2, 2), (4, 2, 8), (8, 16, 4), (32, 4, 2), (64, 64, 32), (128, 2, 4), (2, 128, 32)])
+@pytest.mark.parametrize("N", [(2, 2, 2), (4, 2, 8), (8, 16, 4), (32, 4, 2), (64, 64, 32), (128, 2, 4), (2, 128, 32),
+                               (32, 32, 2), (32, 64, 4), (64, 32, 8), (128, 32, 4), (32, 128, 2), (32, 32, 32)])
 def test_translate_shapes_dense_random(fm, ctx, N):
     """Every FFT path (single pass <= 32, four-step 64..256, z split S = 2 at
-    n3 = 64) on random operators, ragged direction counts, vs the oracle's
-    FP64 FFT path and, on small grids, the O(N^2) direct sum."""
+    n3 = 64; the whole-plane xy kernels for n1, n2 >= 64 with 1, 2 and 4 planes
+    per CTA, including a ragged last CTA: 64 x 64 x 4 has 6 planes) on random
+    operators, ragged direction counts, vs the oracle's FP64 FFT path and, on
+    small grids, the O(N^2) direct sum."""
     rng = np.random.default_rng(sum(N))
     n = tuple(2 * x for x in N)
     nd = 3
