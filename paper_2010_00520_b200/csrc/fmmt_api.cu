@@ -1199,41 +1199,18 @@ static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq) {
   if constexpr (N3 == 64) {
     // all 64 kz per tile, one CTA per SM (PkwCfg); shared A (TT-4D T1): 2-CTA clusters, each A chunk
     // streamed once per pair and multicast
-    if (MODE == fmmt::Z_LOWRANK && ctx->z_wstage) {
-      // W tiles staged through shared memory by TMA (k_pk_conv_z64w); shared A (TT-4D T1): 2-CTA clusters
-      const bool sh = a.g_stride == 0 && a.gp_stride == 0;
-      const bool clw = sh && ctx->z_cluster && nq > 1;
-      const int CLW = clw ? 2 : 1;
-      const int SMW = sh ? fmmt::PkzwCfg<fmmt::PKZW_NS_SH>::SMEM : fmmt::PkzwCfg<fmmt::PKZW_NS>::SMEM;
-      auto kw = clw ? fmmt::k_pk_conv_z64w<fmmt::PKZW_NS_SH, 2>
-                    : (sh ? fmmt::k_pk_conv_z64w<fmmt::PKZW_NS_SH, 1> : fmmt::k_pk_conv_z64w<fmmt::PKZW_NS, 1>);
-      FMMT_CUDA(ctx, set_smem_once((const void*)kw, SMW));
-      const int64_t groups = tiles_m * (int64_t)((nq + CLW - 1) / CLW);
-      const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CLW));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(CLW * ncl);
-      cfg.blockDim = dim3(fmmt::PKZW_THREADS);
-      cfg.dynamicSmemBytes = SMW;
-      cfg.stream = ctx->stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = CLW;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = clw ? 1 : 0;
-      FMMT_CUDA(ctx, cudaLaunchKernelEx(&cfg, kw, a, nq));
-      return FMMT_OK;
-    }
-    // operand ring depth: PKW_NS (10) stages of 16 KB, or 12 (FMMT_ZNS=12: the deepest that fits next to X; A/B)
-    const bool deep = ctx->z_ns == 12;
-    const int SM = deep ? fmmt::PkwCfg<12>::SMEM : fmmt::PkwCfg<fmmt::PKW_NS>::SMEM;
-    const bool cl = ctx->z_cluster && a.g_stride == 0 && a.gp_stride == 0 && nq > 1;
+    constexpr int SM = fmmt::PkwCfg<fmmt::PKW_NS>::SMEM;
+    const bool sh = a.g_stride == 0 && a.gp_stride == 0;
+    const bool cl = ctx->z_cluster && sh && nq > 1;
     const int CL = cl ? 2 : 1;
     const int64_t groups = tiles_m * (int64_t)((nq + CL - 1) / CL);
     const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CL));
-    auto kfn = deep ? (cl ? fmmt::k_pk_conv_z64<MODE, 12, 2> : fmmt::k_pk_conv_z64<MODE, 12, 1>)
-                    : (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>);
+    // shared A (TT-4D T1, K = r2 up to 1201): flush groups of 2 TC_FC K-chunks (the MMA warp runs twice as far
+    // ahead of the per-tile z-DFT epilogue; FMMT_ZFC=4 for TC_FC)
+    const bool longfc = sh && ctx->z_fc != fmmt::TC_FC;
+    auto kfn = longfc ? (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2, 2 * fmmt::TC_FC>
+                            : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1, 2 * fmmt::TC_FC>)
+                      : (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>);
     FMMT_CUDA(ctx, set_smem_once((const void*)kfn, SM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * ncl);
@@ -1588,9 +1565,8 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_W_MB")) ctx->w_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_ZCLUSTER")) ctx->z_cluster = atoi(e) != 0;
   if (const char* e = getenv("FMMT_XY_BIG")) xy_big_enabled = atoi(e) != 0;
-  if (const char* e = getenv("FMMT_ZWSTAGE")) ctx->z_wstage = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZFUSE")) ctx->z_fuse = atoi(e) != 0;
-  if (const char* e = getenv("FMMT_ZNS")) ctx->z_ns = atoi(e);
+  if (const char* e = getenv("FMMT_ZFC")) ctx->z_fc = atoi(e);
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (world > 1) {

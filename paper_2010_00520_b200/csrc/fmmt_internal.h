@@ -29,9 +29,8 @@ struct fmmt_ctx {
   bool use_graphs = true;           // replay whole matvecs as CUDA graphs (see run_graphed)
   int tc_ctas_per_sm = 2;           // tensor-core GEMM grid: CTAs per SM = the resident count (each loops over tiles)
   int batch_mb = 2048;              // per-batch intermediate budget of the 3D formats (FMMT_BATCH_MB)
-  int z_ns = 10;                    // n3 = 64 z-stage operand ring stages: 10 or 12 (FMMT_ZNS)
+  int z_fc = 8;                     // shared-A n3 = 64 z-stage flush group in K-chunks (2 TC_FC; FMMT_ZFC=4: TC_FC)
   bool z_fuse = true;               // Tucker-3D at n3 = 64, n1 % 128 == 0: fused mode-1 / mode-3 z-stage (FMMT_ZFUSE)
-  bool z_wstage = false;            // n3 = 64 z-stage: W tiles staged by TMA (FMMT_ZWSTAGE=1; measured slower, A/B only)
   bool z_cluster = true;            // shared-A n3 = 64 z-stage in 2-CTA clusters with multicast A (FMMT_ZCLUSTER)
   int w_mb = 128;                   // half-padded spectra per xy sub-batch (FMMT_W_MB; 16-128 measured within 4 %)
   int tc_ctas_z = 4;                // tensor-core z-stage grid: CTAs per SM (two waves measured faster there)

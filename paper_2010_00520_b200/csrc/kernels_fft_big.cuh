@@ -240,4 +240,5 @@ k_inv_xy_big(const float2* __restrict__ W, float2* __restrict__ sig_out, int npl
   }
 }
 
+
 }  // namespace fmmt

@@ -198,37 +198,28 @@ __global__ void __launch_bounds__(ZF_THREADS, 1) k_tucker_zf(ZfArgs a, int nq) {
       const int nkc1 = (r1 + TC_BK - 1) / TC_BK;
       const float2* Hj = hs;
       tc::mbar_wait(HFULL, (uint32_t)(i & 1));           // H'_j of tile i staged
-      const int items = nkc1 * 4 * 64;
-      constexpr int UNR = 4;
-      for (int e0 = et; e0 < items; e0 += 256 * UNR) {
-        float2 b0[UNR], b1[UNR];
+      // item (B' row r = 2c + parity, K-chunk kc, K-half): 4 consecutive a -> one 16-byte row piece of hi and of lo;
+      // consecutive threads take consecutive rows, so each quarter-warp stores 128 contiguous bytes
+      const int items = nkc1 * 2 * NR;
+      for (int e = et; e < items; e += 256) {
+        const int r = e & (NR - 1), half = (e >> 7) & 1, kc = e >> 8;
+        const int cc = r >> 1, par = r & 1;
+        const int a0 = kc * TC_BK + 4 * half;
+        float2 b[4];
 #pragma unroll
-        for (int uu = 0; uu < UNR; ++uu) {
-          const int e = e0 + uu * 256;
-          const int cc = e & 63, kp = (e >> 6) & 3, kc = e >> 8;
-          const int a0 = kc * TC_BK + 2 * kp;
-          const bool ok = e < items && cc < r3;
-          b0[uu] = ok && a0 < r1 ? Hj[cc + (int64_t)r3 * a0] : make_float2(0.f, 0.f);
-          b1[uu] = ok && a0 + 1 < r1 ? Hj[cc + (int64_t)r3 * (a0 + 1)] : make_float2(0.f, 0.f);
-        }
+        for (int t = 0; t < 4; ++t)
+          b[t] = (cc < r3 && a0 + t < r1) ? Hj[cc + (int64_t)r3 * (a0 + t)] : make_float2(0.f, 0.f);
+        uint4 hi, lo;
+        uint32_t* hp = reinterpret_cast<uint32_t*>(&hi);
+        uint32_t* lp = reinterpret_cast<uint32_t*>(&lo);
 #pragma unroll
-        for (int uu = 0; uu < UNR; ++uu) {
-          const int e = e0 + uu * 256;
-          if (e < items) {
-            const int cc = e & 63, kp = (e >> 6) & 3, kc = e >> 8;
-            uint2 h0, l0, h1, l1;
-            tc::split_f16x2(b0[uu].x * sH, -b0[uu].y * sH, h0.x, l0.x);
-            tc::split_f16x2(b1[uu].x * sH, -b1[uu].y * sH, h0.y, l0.y);
-            tc::split_f16x2(b0[uu].y * sH, b0[uu].x * sH, h1.x, l1.x);
-            tc::split_f16x2(b1[uu].y * sH, b1[uu].x * sH, h1.y, l1.y);
-            uint8_t* blk = region + kc * ZfCfg::CHUNK;
-            const int off = (2 * cc) * 16 + (kp >> 1) * ZfCfg::LBO_B + (kp & 1) * 8;
-            *reinterpret_cast<uint2*>(blk + off) = h0;
-            *reinterpret_cast<uint2*>(blk + off + 16) = h1;
-            *reinterpret_cast<uint2*>(blk + off + NR * 16) = l0;
-            *reinterpret_cast<uint2*>(blk + off + NR * 16 + 16) = l1;
-          }
+        for (int t = 0; t < 4; ++t) {   // row 2c: [Re, -Im], row 2c + 1: [Im, Re] (selects, no divergence)
+          const float x0 = par ? b[t].y : b[t].x, x1 = par ? b[t].x : -b[t].y;
+          tc::split_f16x2(x0 * sH, x1 * sH, hp[t], lp[t]);
         }
+        uint8_t* blk = region + kc * ZfCfg::CHUNK + r * 16 + half * ZfCfg::LBO_B;
+        *reinterpret_cast<uint4*>(blk) = hi;
+        *reinterpret_cast<uint4*>(blk + NR * 16) = lo;
       }
       tc::fence_async_smem();
       tc::named_bar_sync(1, 256);

@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t pk_setup(uint64_t* bar, uint32_t* tslot) {
 // The MMA warp therefore runs into tile i+1 (other TMEM slot) while warps 0-3 drain and finish tile i.
 constexpr int PK_THREADS = 192;
 
-template <int BN, int NS, class TileOf, class Epi, int CL = 1, int EG = 1>
+template <int BN, int NS, class TileOf, class Epi, int CL = 1, int EG = 1, int FC = TC_FC>
 __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint8_t* sm, uint64_t* bar, uint32_t tmem) {
   using Cfg = PkCfg<BN, NS>;
   constexpr int NR = Cfg::NR;
@@ -142,7 +142,7 @@ __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint
       for (int kc = 0; kc < nk; ++kc, ++c) {
         const int s = (int)(c % NS);
         tc::mbar_wait_addr(DATA(s), (uint32_t)((c / NS) & 1));
-        const bool fresh = kc % TC_FC == 0;
+        const bool fresh = kc % FC == 0;
         if (fresh && g >= 2) tc::mbar_wait_addr(TFREE(g & 1), (uint32_t)(((g >> 1) - 1) & 1));
         __syncwarp();
         tc::fence_after_sync();
@@ -161,7 +161,7 @@ __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint
         }
         if constexpr (CL == 1) tc::mma_commit_el(MMA(s));
         else tc::mma_commit_mc_el(MMA(s), 0x3);            // frees the stage in both CTAs of the pair
-        if (kc % TC_FC == TC_FC - 1 || kc == nk - 1) {   // group g closed
+        if (kc % FC == FC - 1 || kc == nk - 1) {   // group g closed
           tc::mma_commit_el(GDONE(g & 1));
           ++g;
         }
@@ -177,7 +177,7 @@ __device__ __forceinline__ void pk_run(int ntiles, TileOf tile_of, Epi epi, uint
       if (nk <= 0) continue;
 #pragma unroll
       for (int j = 0; j < NRG; ++j) acc[j] = 0.f;
-      const int ngr = (nk + TC_FC - 1) / TC_FC;
+      const int ngr = (nk + FC - 1) / FC;
       for (int q = 0; q < ngr; ++q, ++g) {
         tc::mbar_wait_addr(GDONE(g & 1), (uint32_t)((g >> 1) & 1));
         tc::fence_after_sync();
@@ -349,7 +349,9 @@ struct PkwCfg {
   static constexpr int SMEM = Cfg::SMEM + X_BYTES;
 };
 
-template <int MODE, int NS, int CL = 1>
+// FC: K-chunks per TMEM flush group (TC_FC; 2 TC_FC = FMMT_ZFC=8 for the long-K shared-A TT-4D stage lets the MMA
+// warp run twice as far ahead of the per-tile z-DFT epilogue, at twice the chained truncating adds per group)
+template <int MODE, int NS, int CL = 1, int FC = TC_FC>
 __global__ void __launch_bounds__(PKW_THREADS, 1) k_pk_conv_z64(ZArgs a, int nq) {
   constexpr int N3 = 64, H = 32, BN = 64;
   using Cfg = PkCfg<BN, NS>;
@@ -421,139 +423,7 @@ __global__ void __launch_bounds__(PKW_THREADS, 1) k_pk_conv_z64(ZArgs a, int nq)
       }
     }
   };
-  pk_run<BN, NS, decltype(tile_of), decltype(epi), CL, 2>(ntiles, tile_of, epi, pksm, bar, tmem);
-  pk_teardown<BN, NS, CL, 2>(tmem);
-}
-
-// ---------------------------------------------------------------- k_pk_conv_z64w (n3 = 64, W staged)
-// The n3 = 64 z-stage of k_pk_conv_z64 with the half-padded spectra staged through shared memory by the TMA
-// engine: a loader warp (warp 10) bulk-copies the next unit's W tile (32 z-rows x 128 lines of one (tile,
-// component)) into one of two 32 KB buffers while the epilogue warps transform the current one; the epilogue
-// reads its line from shared memory, exchanges the odd-kz half in the same buffer, and one thread bulk-stores
-// the result rows back to W.  The epilogue warps never wait on global-memory latency (k_pk_conv_z64 loads its
-// 32 W values per line straight from L2 / HBM), which shortens the per-tile epilogue during which the MMA warp
-// can run only two flush groups ahead (two TMEM slots).
-// CL = 2 (shared A, TT-4D T1): 2-CTA clusters, A multicast, as k_pk_conv_z64; ghost halves of an odd
-// direction count skip their epilogue and their W unit.
-// Warps: 0-7 drain + epilogue (EG = 2), 8 MMA issuer, 9 operand producer, 10 W loader.
-constexpr int PKZW_THREADS = 352;
-constexpr int PKZW_NS = 8;      // per-direction A (3D formats, Tucker-4D, H-Tucker)
-constexpr int PKZW_NS_SH = 10;  // shared A (TT-4D): the deepest ring that fits next to the two W buffers
-template <int NS>
-struct PkzwCfg {
-  using Cfg = PkCfg<64, NS>;
-  static constexpr int WB = TC_BM * 32 * 8;          // one W unit: 32 z-rows x 128 lines
-  static constexpr int SMEM = Cfg::SMEM + 2 * WB;
-};
-
-template <int NS, int CL>
-__global__ void __launch_bounds__(PKZW_THREADS, 1) k_pk_conv_z64w(ZArgs a, int nq) {
-  constexpr int N3 = 64, H = 32, BN = 64;
-  using Cfg = PkCfg<BN, NS>;
-  extern __shared__ __align__(1024) uint8_t pksm[];
-  __shared__ __align__(8) uint64_t bar[Cfg::NBAR];
-  __shared__ __align__(8) uint64_t wbar[4];          // wfull[2], wfree[2]
-  __shared__ uint32_t tslot;
-  float2* Wbuf = reinterpret_cast<float2*>(pksm + Cfg::SMEM);
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&wbar[0], 1);
-    tc::mbar_init(&wbar[1], 1);
-    tc::mbar_init(&wbar[2], 1);
-    tc::mbar_init(&wbar[3], 1);
-  }
-  const uint32_t tmem = pk_setup<BN, NS, CL, 2>(bar, &tslot);   // (its __syncthreads publishes wbar too)
-  const int tiles_m = (int)((a.n12 + TC_BM - 1) / TC_BM);
-  const int nqc = (nq + CL - 1) / CL;                    // direction groups (pairs when CL = 2)
-  const int total = tiles_m * nqc;
-  const int cid = (int)blockIdx.x / CL, ncl = (int)gridDim.x / CL, crank = (int)blockIdx.x % CL;
-  const int ntiles = total > cid ? (total - cid + ncl - 1) / ncl : 0;
-  const bool shared_a = a.g_stride == 0 && a.gp_stride == 0;
-  // tile i of this CTA: direction q (>= nq: the ghost half of the last pair), m-tile mt
-  auto coords = [&](int i, int& q, int& mt) {
-    z_tile(cid + i * ncl, tiles_m, nqc, shared_a && a.z_blocked, q, mt);
-    q = q * CL + crank;
-  };
-  auto nk_of = [&](int q) {
-    const int k = a.rank_p ? a.rank_p[a.p0 + q] : a.rank;
-    return (k + TC_BK - 1) / TC_BK;
-  };
-  auto tile_of = [&](int i) -> PkTile {
-    int q, mt;
-    coords(i, q, mt);
-    q = min(q, nq - 1);                                  // a ghost streams (and multicasts) like its pair
-    const int nkc = nk_of(q);
-    PkTile t;
-    t.apk = a.Gp + (int64_t)q * a.gp_stride + (int64_t)mt * nkc * TC_PACK_FLOATS;
-    t.bpk = a.Vp + (a.vp_off ? a.vp_off[a.p0 + q] : (int64_t)q * a.vp_stride);
-    t.nk = nkc;
-    return t;
-  };
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 10) {   // ------------------------------------------------------------- W loader
-    int u = 0;
-    for (int i = 0; i < ntiles; ++i) {
-      int q, mt;
-      coords(i, q, mt);
-      if (q >= nq || nk_of(q) <= 0) continue;
-      const int rows = (int)(a.n12 - (int64_t)mt * TC_BM < TC_BM ? a.n12 - (int64_t)mt * TC_BM : TC_BM);
-      for (int cc = 0; cc < a.ncomp; ++cc, ++u) {
-        const int b = u & 1, n = u >> 1;
-        if (n >= 1) tc::mbar_wait(&wbar[2 + b], (uint32_t)((n - 1) & 1));
-        if (lane == 0) tc::mbar_expect_tx(&wbar[b], (uint32_t)(H * rows * 8));
-        __syncwarp();
-        const float2* src = a.W + ((int64_t)(q * a.ncomp + cc) * H + lane) * a.n12 + (int64_t)mt * TC_BM;
-        tc::bulk_g2s(tc::smem_u32(Wbuf + b * (H * TC_BM) + lane * TC_BM), src, (uint32_t)(rows * 8), &wbar[b]);
-      }
-    }
-  }
-  const float sB0 = (TC_F16 && a.bmax) ? tc::f16_scale(*a.bmax) : 1.f;
-  const float sA0 = (TC_F16 && a.amax) ? tc::f16_scale(*a.amax) : 1.f;
-  const float inv = 1.f / (sA0 * sB0);
-  int u = 0;   // epilogue unit counter (same order as the loader's)
-  auto epi = [&](int i, float (&acc)[Cfg::NR / 2], int h) {
-    int q, mt;
-    coords(i, q, mt);
-    if (q >= nq) return;                                 // ghost half: no W unit
-    const int row = threadIdx.x & (TC_BM - 1);
-    const int rows = (int)(a.n12 - (int64_t)mt * TC_BM < TC_BM ? a.n12 - (int64_t)mt * TC_BM : TC_BM);
-    for (int cc = 0; cc < a.ncomp; ++cc, ++u) {
-      const int b = u & 1, n = u >> 1;
-      float2* Wb = Wbuf + b * (H * TC_BM);
-      tc::mbar_wait(&wbar[b], (uint32_t)(n & 1));
-      float2 f[H];
-#pragma unroll
-      for (int z = 0; z < H; ++z) f[z] = Wb[z * TC_BM + row];
-      if (h) {
-#pragma unroll
-        for (int z = 1; z < H; ++z) f[z] = cmul(f[z], twc<N3, false>(z));
-      }
-      fft_reg<H, false, false>(f);
-#pragma unroll
-      for (int m = 0; m < H; ++m) f[m] = cmul2(f[m], make_float2(acc[2 * m] * inv, acc[2 * m + 1] * inv));
-      fft_reg<H, true, false>(f);
-      tc::named_bar_sync(1, 256);                      // both groups have read the unit's W lines
-      if (h) {
-#pragma unroll
-        for (int z = 0; z < H; ++z) Wb[z * TC_BM + row] = z ? cmul(f[z], twc<N3, true>(z)) : f[z];
-      }
-      tc::named_bar_sync(1, 256);                      // the odd half is in the buffer
-      if (!h) {
-#pragma unroll
-        for (int z = 0; z < H; ++z) Wb[z * TC_BM + row] = cadd(f[z], Wb[z * TC_BM + row]);
-        tc::fence_async_smem();                        // generic-proxy writes -> the bulk-copy engine
-        tc::named_bar_sync(2, 128);
-        if (threadIdx.x == 0) {
-          float2* dst = a.W + (int64_t)(q * a.ncomp + cc) * H * a.n12 + (int64_t)mt * TC_BM;
-          for (int z = 0; z < H; ++z) tc::bulk_s2g(dst + (int64_t)z * a.n12, tc::smem_u32(Wb + z * TC_BM), (uint32_t)(rows * 8));
-          tc::bulk_commit();
-          tc::bulk_wait_read0();                       // buffer b may be refilled
-          tc::mbar_arrive(&wbar[2 + b]);
-        }
-      }
-    }
-  };
-  pk_run<BN, NS, decltype(tile_of), decltype(epi), CL, 2>(ntiles, tile_of, epi, pksm, bar, tmem);
-  if (threadIdx.x == 0) tc::bulk_wait0();
+  pk_run<BN, NS, decltype(tile_of), decltype(epi), CL, 2, FC>(ntiles, tile_of, epi, pksm, bar, tmem);
   pk_teardown<BN, NS, CL, 2>(tmem);
 }
 
