@@ -1206,11 +1206,13 @@ static fmmt_status launch_pk_z(fmmt_ctx* ctx, const ZArgs& a, int nq) {
     const int64_t groups = tiles_m * (int64_t)((nq + CL - 1) / CL);
     const unsigned ncl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms / CL));
     // shared A (TT-4D T1, K = r2 up to 1201): flush groups of 2 TC_FC K-chunks (the MMA warp runs twice as far
-    // ahead of the per-tile z-DFT epilogue; FMMT_ZFC=4 for TC_FC)
-    const bool longfc = sh && ctx->z_fc != fmmt::TC_FC;
-    auto kfn = longfc ? (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2, 2 * fmmt::TC_FC>
-                            : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1, 2 * fmmt::TC_FC>)
-                      : (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>);
+    // ahead of the per-tile z-DFT epilogue; FMMT_ZFC=4 for TC_FC, 16 for 4 TC_FC)
+    const int fcm = !sh ? 1 : ctx->z_fc >= 4 * fmmt::TC_FC ? 4 : ctx->z_fc >= 2 * fmmt::TC_FC ? 2 : 1;
+    auto kfn = fcm == 4 ? (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2, 4 * fmmt::TC_FC>
+                              : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1, 4 * fmmt::TC_FC>)
+             : fcm == 2 ? (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2, 2 * fmmt::TC_FC>
+                              : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1, 2 * fmmt::TC_FC>)
+                        : (cl ? fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 2> : fmmt::k_pk_conv_z64<MODE, fmmt::PKW_NS, 1>);
     FMMT_CUDA(ctx, set_smem_once((const void*)kfn, SM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * ncl);

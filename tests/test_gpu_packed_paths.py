@@ -147,10 +147,10 @@ def test_n3_64_per_direction_a_matches_oracle(fm, fmt, ncomp, nxy):
     ctx.close()
 
 
-@pytest.mark.parametrize("fc", [4, 8])
+@pytest.mark.parametrize("fc", [4, 8, 16])
 def test_tt4d_flush_group_lengths_agree(fm, fc):
-    """TT-4D n3 = 64 z-stage with TMEM flush groups of 4 and 8 K-chunks (FMMT_ZFC; 8 is the default for the
-    shared-A stage): both match the oracle at the translate bar."""
+    """TT-4D n3 = 64 z-stage with TMEM flush groups of 4, 8 and 16 K-chunks (FMMT_ZFC; 8 is the default for
+    the shared-A stage): all match the oracle at the translate bar."""
     cp, _ = _n64_operator("tt4d", 1e-4)
     ctx = _ctx_env(fm, FMMT_ZFC=fc)
     _check_multi(ctx, cp, (4, 4, 32), 2, 500 + fc)
