@@ -27,6 +27,7 @@
 
 #include "fmmt_internal.h"
 #include "kernels_agg.cuh"
+#include "kernels_dense.cuh"
 #include "kernels_fft.cuh"
 #include "kernels_fft_big.cuh"
 #include "kernels_gemm.cuh"
@@ -223,8 +224,9 @@ ZKernel make_z(int mode) {
   constexpr int S = (N3 <= 32) ? 1 : 2;
   ZKernel k;
   k.S = S;
-  if (mode == fmmt::Z_DENSE) k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_DENSE>;
-  else if (mode == fmmt::Z_LOWRANK) k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_LOWRANK>;
+  if (mode == fmmt::Z_DENSE) {
+    k.fn = fmmt::k_conv_z_dense<N3, S>;
+  } else if (mode == fmmt::Z_LOWRANK) k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_LOWRANK>;
   else k.fn = fmmt::k_conv_z<N3, S, fmmt::Z_RESTORE>;
   return k;
 }
