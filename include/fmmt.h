@@ -76,7 +76,10 @@ fmmt_status fmmt_init(int device, void* cuda_stream, fmmt_ctx** ctx);
 /* Create a context that is rank `rank` of `world` direction shards.  The
  * 128-byte NCCL unique id comes from fmmt_nccl_unique_id() on rank 0 and is
  * distributed by the caller (e.g. a torch.distributed broadcast).  All ranks
- * must call this collectively.  world == 1 needs no id (may be NULL).       */
+ * must call this collectively.  world == 1 needs no id (may be NULL); given
+ * one, it creates a single-rank communicator and every collective of the
+ * sharded path (the 4D setup broadcast, the per-matvec allreduce) still runs,
+ * which is how the NCCL call sequence is exercised on a one-GPU box.        */
 fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world,
                               const void* nccl_unique_id, fmmt_ctx** ctx);
 fmmt_status fmmt_nccl_unique_id(void* out_128_bytes);
@@ -220,6 +223,19 @@ fmmt_status fmmt_op_info(const fmmt_op* op, fmmt_op_info_t* info);
  * FMMT_E_CUDA (copy).                                                            */
 fmmt_status fmmt_op_export(const fmmt_op* op, int64_t index, fmmt_c64* dst, int64_t cap, int64_t* count);
 
+/* Optional op serialisation (SURVEY.md §5 "checkpoint / resume": skip the
+ * setup-time compression of Alg. 1-3, on later runs).
+ * fmmt_op_save writes the op's ranks and complex64 factor arrays (exactly what
+ * fmmt_op_ranks / fmmt_op_export return, so a sharded op saves its own shard)
+ * to `path` (host file, overwritten); fmmt_op_load re-creates an op from such a
+ * file on `ctx` as fmmt_op_import would (derived operands and plans are rebuilt;
+ * shapes outside the translate path load as storage-only ops).  A loaded op's
+ * translate / restore output is bit-identical to the saved op's.
+ * Errors: FMMT_E_ARG (null), FMMT_E_STATE (I/O failure, not an op file,
+ * truncated, checksum mismatch), otherwise as fmmt_op_export / fmmt_op_import. */
+fmmt_status fmmt_op_save(const fmmt_op* op, const char* path);
+fmmt_status fmmt_op_load(fmmt_ctx* ctx, const char* path, fmmt_op** op);
+
 /* Ranks: 3D formats write [ndir][nslots] (per direction), 4D formats nslots.
  * *count = number of int64 written (fails with FMMT_E_ARG if cap is short). */
 fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_t* count);
@@ -273,7 +289,10 @@ fmmt_status fmmt_translate_sum_multi(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c
 /* End-to-end variant on HOST buffers: copies sig_in (host, [ndir][Nz][Ny][Nx])
  * and w (host) to the device, runs fmmt_translate_sum, copies the summed
  * result to sum_out (host [Nz][Ny][Nx]) and synchronises the stream.
- * Pinned host memory gives asynchronous copies.                             */
+ * Pinned host memory gives asynchronous copies: the signatures are uploaded
+ * in chunks of directions on a copy stream and each chunk is awaited only by
+ * the first kernel that reads it, so the upload overlaps the restore GEMMs
+ * and the earlier sub-batches (FMMT_H2D_OVERLAP=0: one serial copy first).   */
 fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, const float* w_host,
                                     fmmt_c64* sum_out_host, int64_t ndir,
                                     int64_t Nx, int64_t Ny, int64_t Nz);

@@ -333,6 +333,11 @@ struct fmmt_op {
   float2* d_in_host = nullptr;   // device buffer for e2e input
   float* d_w_host = nullptr;
   float2* d_sum_host = nullptr;
+  // overlapped upload (fmmt_translate_sum_host): events of the chunks of h2d_chunk directions, waited on by
+  // translate_impl just before the first kernel that reads a chunk's signatures
+  const cudaEvent_t* h2d_ev = nullptr;
+  int64_t h2d_chunk = 0;
+  int h2d_nchunks = 0, h2d_waited = 0;
   // far-field matvec (fmmt_far_matvec): aggregated and translated signatures [ndir][ncomp][K]
   float* Vpk = nullptr;                         // TT-4D z-stage: pre-split V_q of a batch (k_tc_pack_b)
   int64_t vpk_floats = 0;
@@ -1419,6 +1424,11 @@ static fmmt_status translate_impl(fmmt_op* op, const fmmt_c64* sig_in, fmmt_c64*
       const int sn = (int)std::min<int64_t>(op->SB, b.nq - s0);
       const int64_t p = b.q0 + s0;
       const int planes = sn * ncomp * Nz;
+      if (op->h2d_ev) {   // host path: the upload of these directions' chunks must have landed
+        const int c = (int)std::min<int64_t>((p + sn - 1) / op->h2d_chunk, op->h2d_nchunks - 1);
+        for (; op->h2d_waited <= c; ++op->h2d_waited)
+          FMMT_CUDA(op->ctx, cudaStreamWaitEvent(op->ctx->stream, op->h2d_ev[op->h2d_waited], 0));
+      }
       if ((st = launch_xy(op, true, in + p * ncomp * K, op->W, planes, 1.f))) return st;
       if ((st = launch_z(op, mode, (int)p, s0, sn, nullptr, op->W, ncomp))) return st;
       if ((st = launch_xy(op, false, op->W, out + p * ncomp * K, planes, scale))) return st;
@@ -1571,9 +1581,10 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_XY_BIG")) xy_big_enabled = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZFUSE")) ctx->z_fuse = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZFC")) ctx->z_fc = atoi(e);
+  if (const char* e = getenv("FMMT_H2D_OVERLAP")) ctx->h2d_overlap = atoi(e) != 0;
   if (const char* e = getenv("FMMT_TC_CTAS_Z")) ctx->tc_ctas_z = std::max(1, atoi(e));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (world > 1) {
+  if (world > 1 || nccl_id) {   // world == 1 with an id: a single-rank communicator (the collective paths still run)
     ncclUniqueId id;
     memcpy(&id, nccl_id, 128);
     ncclComm_t comm;
@@ -1597,6 +1608,12 @@ void fmmt_destroy(fmmt_ctx* ctx) {
     cudaEventDestroy(pe.e1);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  for (auto e : ctx->h2d_events) cudaEventDestroy(e);
+  if (ctx->h2d_fence) cudaEventDestroy(ctx->h2d_fence);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
   if (ctx->agg_part) cudaFree(ctx->agg_part);
   fmmt_internal::setup_release(ctx);
@@ -1786,6 +1803,86 @@ fmmt_status fmmt_op_ranks(const fmmt_op* op, int64_t* ranks, int64_t cap, int64_
   return FMMT_OK;
 }
 
+// ---------------------------------------------------------------- op serialisation (skip re-compression)
+// File: magic "FMMTOP\1\0", int64 {format, n1, n2, n3, ndir, nranks, narrays}, int64 ranks[nranks], then per
+// array int64 count + count complex64 (the fmmt_op_import order and layout), then a uint64 checksum of the array
+// payload.  Little-endian, as the host writes it.
+static const char OP_MAGIC[8] = {'F', 'M', 'M', 'T', 'O', 'P', 1, 0};
+
+static uint64_t payload_sum(uint64_t h, const void* data, size_t bytes) {
+  const uint64_t* w = static_cast<const uint64_t*>(data);   // complex64 payloads: multiples of 8 bytes
+  for (size_t i = 0; i < bytes / 8; ++i) h = ((h << 7) | (h >> 57)) ^ (w[i] * 0x9E3779B97F4A7C15ull);
+  return h;
+}
+
+fmmt_status fmmt_op_save(const fmmt_op* op, const char* path) {
+  if (!op) return FMMT_E_ARG;
+  fmmt_ctx* ctx = op->ctx;
+  CHECK_ARG(ctx, path && *path, "null path");
+  FILE* f = fopen(path, "wb");
+  if (!f) return set_err(ctx, FMMT_E_STATE, "cannot open %s for writing", path);
+  const int64_t hdr[7] = {(int64_t)op->format, op->n1, op->n2, op->n3, op->ndir, (int64_t)op->ranks.size(),
+                          (int64_t)op->arr.size()};
+  bool ok = fwrite(OP_MAGIC, 1, 8, f) == 8 && fwrite(hdr, 8, 7, f) == 7 &&
+            fwrite(op->ranks.data(), 8, op->ranks.size(), f) == op->ranks.size();
+  uint64_t sum = 0;
+  std::vector<float2> host;
+  fmmt_status st = FMMT_OK;
+  for (size_t i = 0; ok && !st && i < op->arr.size(); ++i) {
+    int64_t cnt = 0;
+    host.resize((size_t)std::max<int64_t>(1, op->arr_elems[i]));
+    st = fmmt_op_export(op, (int64_t)i, reinterpret_cast<fmmt_c64*>(host.data()), (int64_t)host.size(), &cnt);
+    if (st) break;
+    ok = fwrite(&cnt, 8, 1, f) == 1 && fwrite(host.data(), 8, (size_t)cnt, f) == (size_t)cnt;
+    sum = payload_sum(sum, host.data(), (size_t)cnt * 8);
+  }
+  ok = ok && !st && fwrite(&sum, 8, 1, f) == 1;
+  ok = (fclose(f) == 0) && ok;
+  if (st) return st;
+  if (!ok) return set_err(ctx, FMMT_E_STATE, "short write to %s", path);
+  return FMMT_OK;
+}
+
+fmmt_status fmmt_op_load(fmmt_ctx* ctx, const char* path, fmmt_op** out) {
+  if (!ctx || !out) return FMMT_E_ARG;
+  *out = nullptr;
+  CHECK_ARG(ctx, path && *path, "null path");
+  FILE* f = fopen(path, "rb");
+  if (!f) return set_err(ctx, FMMT_E_STATE, "cannot open %s", path);
+  struct Closer {
+    FILE* f;
+    ~Closer() { fclose(f); }
+  } closer{f};
+  char magic[8];
+  int64_t hdr[7];
+  if (fread(magic, 1, 8, f) != 8 || memcmp(magic, OP_MAGIC, 8) != 0 || fread(hdr, 8, 7, f) != 7)
+    return set_err(ctx, FMMT_E_STATE, "%s is not an fmmt op file", path);
+  const int64_t format = hdr[0], ndir = hdr[4], nranks = hdr[5], narr = hdr[6];
+  if (format < FMMT_DENSE || format > FMMT_TT4D || ndir < 1 || nranks < 0 || nranks > 6 * ndir || narr < 1 || narr > 8)
+    return set_err(ctx, FMMT_E_STATE, "%s: bad header", path);
+  std::vector<int64_t> ranks((size_t)nranks);
+  if (fread(ranks.data(), 8, (size_t)nranks, f) != (size_t)nranks) return set_err(ctx, FMMT_E_STATE, "%s: truncated", path);
+  fseek(f, 0, SEEK_END);
+  const int64_t fsize = (int64_t)ftell(f);
+  fseek(f, 8 + 7 * 8 + nranks * 8, SEEK_SET);
+  std::vector<std::vector<float2>> arrays((size_t)narr);
+  std::vector<const void*> ptrs((size_t)narr);
+  uint64_t sum = 0;
+  for (int64_t i = 0; i < narr; ++i) {
+    int64_t cnt = -1;
+    if (fread(&cnt, 8, 1, f) != 1 || cnt < 0 || cnt * 8 > fsize) return set_err(ctx, FMMT_E_STATE, "%s: truncated", path);
+    arrays[i].resize((size_t)std::max<int64_t>(1, cnt));
+    if (fread(arrays[i].data(), 8, (size_t)cnt, f) != (size_t)cnt) return set_err(ctx, FMMT_E_STATE, "%s: truncated", path);
+    sum = payload_sum(sum, arrays[i].data(), (size_t)cnt * 8);
+    ptrs[i] = arrays[i].data();
+  }
+  uint64_t stored = 0;
+  if (fread(&stored, 8, 1, f) != 1 || stored != sum) return set_err(ctx, FMMT_E_STATE, "%s: checksum mismatch", path);
+  // shapes and the rank chain are validated by create_op exactly as for fmmt_op_import
+  return fmmt_internal::create_op(ctx, (fmmt_format)format, hdr[1], hdr[2], hdr[3], ndir, nranks ? ranks.data() : nullptr,
+                                  ptrs.data(), narr, out, true);
+}
+
 fmmt_status fmmt_op_set_batch(fmmt_op* op, int64_t dirs) {
   if (!op || dirs < 0) return FMMT_E_ARG;
   if (!op->translatable) return set_err(op->ctx, FMMT_E_UNSUPPORTED, "storage-only op");
@@ -1845,7 +1942,7 @@ static fmmt_status dirsum_and_reduce(fmmt_op* op, const float2* sig, const float
     fmmt::k_dirsum_final<<<(unsigned)((K + 7) / 8), 256, 0, ctx->stream>>>(op->partial, sum_out, K, nsplit);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
-  if (ctx->world > 1) {
+  if (ctx->nccl_comm) {
     ncclResult_t r = ncclAllReduce(sum_out, sum_out, (size_t)(2 * K), ncclFloat, ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream);
     if (r != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
   }
@@ -1905,11 +2002,63 @@ fmmt_status fmmt_translate_sum_host(fmmt_op* op, const fmmt_c64* sig_in_host, co
         (st = dev_alloc(op, &op->d_sum_host, K * 8, MEM_WORKSPACE, "host staging")))
       return st;
   }
-  FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_in_host, sig_in_host, ndir * K * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
-  FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_w_host, w_host, ndir * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-  fmmt_status st = fmmt_translate_sum(op, reinterpret_cast<const fmmt_c64*>(op->d_in_host), nullptr, op->d_w_host,
-                                      reinterpret_cast<fmmt_c64*>(op->d_sum_host), ndir, Nx, Ny, Nz);
-  if (st) return st;
+  if (!ctx->h2d_overlap || ctx->stream == nullptr || ctx->profiling) {
+    FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_in_host, sig_in_host, ndir * K * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+    FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_w_host, w_host, ndir * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    fmmt_status st = fmmt_translate_sum(op, reinterpret_cast<const fmmt_c64*>(op->d_in_host), nullptr, op->d_w_host,
+                                        reinterpret_cast<fmmt_c64*>(op->d_sum_host), ndir, Nx, Ny, Nz);
+    if (st) return st;
+  } else {
+    // Overlapped upload: the signatures go up in chunks of one xy sub-batch of directions on a copy stream, an
+    // event after each; the matvec is launched directly (no graph) and waits for a chunk only before the first
+    // kernel that reads it (the forward xy FFT of that sub-batch), so the restore GEMMs and the earlier
+    // sub-batches run under the copy.
+    fmmt_status st = ensure_w(op, 1);   // fixes op->SB, the xy sub-batch (the upload chunk)
+    if (st) return st;
+    if (!ctx->copy_stream) {
+      FMMT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      FMMT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->h2d_fence, cudaEventDisableTiming));
+    }
+    const int64_t chunk = std::max<int64_t>(std::max<int64_t>(1, op->SB), (ndir + 63) / 64);
+    const int nchunks = (int)((ndir + chunk - 1) / chunk);
+    while ((int)ctx->h2d_events.size() < nchunks) {
+      cudaEvent_t ev;
+      FMMT_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx->h2d_events.push_back(ev);
+    }
+    // the staging buffer's earlier readers are on ctx->stream
+    FMMT_CUDA(ctx, cudaEventRecord(ctx->h2d_fence, ctx->stream));
+    FMMT_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->h2d_fence, 0));
+    for (int c = 0; c < nchunks; ++c) {
+      const int64_t d0 = c * chunk, dn = std::min<int64_t>(chunk, ndir - d0);
+      FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_in_host + d0 * K, reinterpret_cast<const float2*>(sig_in_host) + d0 * K,
+                                     dn * K * sizeof(float2), cudaMemcpyHostToDevice, ctx->copy_stream));
+      FMMT_CUDA(ctx, cudaEventRecord(ctx->h2d_events[c], ctx->copy_stream));
+    }
+    FMMT_CUDA(ctx, cudaMemcpyAsync(op->d_w_host, w_host, ndir * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    if (!op->sigtmp || op->sigtmp_elems < ndir * K) {
+      drop_graphs(op);
+      dev_free(op, op->sigtmp);
+      if (!(st = cmalloc(op, &op->sigtmp, ndir * K))) op->sigtmp_elems = ndir * K;
+    }
+    if (!st) st = check_translate_args(op, op->d_in_host, op->sigtmp, ndir, Nx, Ny, Nz, 1);
+    if (!st) {
+      NvtxRange nr("fmmt_matvec_host");
+      op->h2d_ev = ctx->h2d_events.data();
+      op->h2d_chunk = chunk;
+      op->h2d_nchunks = nchunks;
+      op->h2d_waited = 0;
+      st = translate_impl(op, reinterpret_cast<const fmmt_c64*>(op->d_in_host), reinterpret_cast<fmmt_c64*>(op->sigtmp), 1);
+      // every chunk is waited on even if a sub-batch loop ended early: the next call reuses the staging buffer
+      for (; op->h2d_waited < nchunks; ++op->h2d_waited) cudaStreamWaitEvent(ctx->stream, op->h2d_ev[op->h2d_waited], 0);
+      op->h2d_ev = nullptr;
+      if (!st) st = dirsum_and_reduce(op, op->sigtmp, op->d_w_host, op->d_sum_host, 1);
+    }
+    if (st) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      return st;
+    }
+  }
   FMMT_CUDA(ctx, cudaMemcpyAsync(sum_out_host, op->d_sum_host, K * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
   FMMT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FMMT_OK;
@@ -2002,7 +2151,7 @@ static fmmt_status disaggregate_impl(fmmt_ctx* ctx, const float2* P, const float
     fmmt::k_disaggregate_final<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(part, N, nsplit, y);
     FMMT_CUDA(ctx, cudaGetLastError());
   }
-  if (ctx->world > 1) {
+  if (ctx->nccl_comm) {
     ncclResult_t r = ncclAllReduce(y, y, (size_t)(2 * N), ncclFloat, ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream);
     if (r != ncclSuccess) return set_err(ctx, FMMT_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
   }

@@ -41,6 +41,10 @@ struct fmmt_ctx {
   std::vector<std::pair<const char*, std::pair<double, int64_t>>> prof;   // name -> (ms, launches)
   std::vector<cudaEvent_t> event_pool;
   std::vector<void*> prof_execs;    // cudaGraphExec_t of profiled matvecs (destroyed at flush)
+  bool h2d_overlap = true;          // fmmt_translate_sum_host: chunked upload on copy_stream, overlapped with the matvec (FMMT_H2D_OVERLAP=0: serial)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t h2d_fence = nullptr;
+  std::vector<cudaEvent_t> h2d_events;   // one per uploaded chunk of directions
   void* blas = nullptr;             // cublasHandle_t (setup only)
   void* solver = nullptr;           // cusolverDnHandle_t (setup only)
 };

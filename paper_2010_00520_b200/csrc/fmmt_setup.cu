@@ -860,7 +860,7 @@ static fmmt_status compress_impl(fmmt_ctx* ctx, const fmmt_c128* T, int64_t n1, 
   const bool is4d = format == FMMT_TUCKER4D || format == FMMT_HTUCKER4D || format == FMMT_TT4D;
   // sharded 4D setup: rank 0 compresses the whole T_4D and broadcasts the shared factors and
   // the direction factor; every rank keeps the rows of its own directions.  Other ranks pass T = NULL.
-  const bool bcast = is4d && ctx->world > 1;
+  const bool bcast = is4d && ctx->nccl_comm != nullptr;
   const bool receiver = bcast && ctx->rank != 0;
   if (!T && !receiver) return set_err(ctx, FMMT_E_ARG, "null T");
   if (!(tol > 0 && tol < 1)) return set_err(ctx, FMMT_E_ARG, "tol must be in (0,1)");
@@ -1080,7 +1080,7 @@ extern "C" fmmt_status fmmt_compress(fmmt_ctx* ctx, const fmmt_c128* T, int64_t 
   bool sent = false;
   fmmt_status st = compress_impl(ctx, T, n1, n2, n3, ndir, dir_begin, dir_count, format, tol, op, &sent);
   const bool is4d = format == FMMT_TUCKER4D || format == FMMT_HTUCKER4D || format == FMMT_TT4D;
-  if (st != FMMT_OK && !sent && ctx && ctx->world > 1 && ctx->rank == 0 && is4d && ctx->nccl_comm) {
+  if (st != FMMT_OK && !sent && ctx && ctx->rank == 0 && is4d && ctx->nccl_comm) {
     // the root failed before its broadcast: send an all-zero rank header so the other ranks return
     // FMMT_E_STATE instead of waiting forever (the root keeps its own error message)
     std::string err = ctx->err;

@@ -75,6 +75,8 @@ fmmt_build_operator_lossy = _sig("fmmt_build_operator_lossy", C.c_int, vp, i64, 
 fmmt_compress = _sig("fmmt_compress", C.c_int, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_double, C.POINTER(vp))
 fmmt_op_import = _sig("fmmt_op_import", C.c_int, vp, C.c_int, i64, i64, i64, i64, i64p, C.POINTER(vp), i64, C.POINTER(vp))
 fmmt_op_destroy = _sig("fmmt_op_destroy", None, vp)
+fmmt_op_save = _sig("fmmt_op_save", C.c_int, vp, C.c_char_p)
+fmmt_op_load = _sig("fmmt_op_load", C.c_int, vp, C.c_char_p, C.POINTER(vp))
 fmmt_op_info = _sig("fmmt_op_info", C.c_int, vp, C.POINTER(fmmt_op_info_t))
 fmmt_op_ranks = _sig("fmmt_op_ranks", C.c_int, vp, i64p, i64, i64p)
 fmmt_op_export = _sig("fmmt_op_export", C.c_int, vp, i64, vp, i64, i64p)
@@ -95,7 +97,7 @@ EXPORTED = [
     "fmmt_version", "fmmt_init", "fmmt_init_sharded", "fmmt_nccl_unique_id", "fmmt_destroy", "fmmt_sync",
     "fmmt_last_error", "fmmt_shard_range", "fmmt_set_profiling", "fmmt_prof_reset", "fmmt_prof_read",
     "fmmt_launch_count", "fmmt_multipole_count", "fmmt_direction_grid", "fmmt_build_operator", "fmmt_compress",
-    "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_export", "fmmt_op_set_batch", "fmmt_translate",
+    "fmmt_op_import", "fmmt_op_destroy", "fmmt_op_info", "fmmt_op_ranks", "fmmt_op_export", "fmmt_op_save", "fmmt_op_load", "fmmt_op_set_batch", "fmmt_translate",
     "fmmt_translate_sum", "fmmt_translate_sum_host", "fmmt_restore", "fmmt_set_gemm_impl", "fmmt_test_cgemm",
     "fmmt_translate_multi", "fmmt_translate_sum_multi", "fmmt_build_operator_lossy",
     "fmmt_aggregate", "fmmt_disaggregate", "fmmt_far_matvec",
@@ -158,7 +160,7 @@ class Context:
     def __init__(self, device: int = 0, stream: int | None = None, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None):
         h = vp()
-        if world == 1:
+        if world == 1 and nccl_id is None:
             st = fmmt_init(device, stream, C.byref(h))
         else:
             idbuf = C.create_string_buffer(nccl_id, 128)
@@ -253,6 +255,11 @@ class Context:
                self.h, "fmmt_op_import")
         return Op(self, h)
 
+    def load_op(self, path) -> "Op":
+        h = vp()
+        _check(fmmt_op_load(self.h, os.fsencode(path), C.byref(h)), self.h, "fmmt_op_load")
+        return Op(self, h)
+
 
 class Op:
     def __init__(self, ctx: Context, h):
@@ -291,6 +298,9 @@ class Op:
             _check(fmmt_op_export(self.h, idx, a.ctypes.data, len(a), C.byref(cnt)), self.ctx.h, "fmmt_op_export")
             out.append(a[:cnt.value])
         return out
+
+    def save(self, path):
+        _check(fmmt_op_save(self.h, os.fsencode(path)), self.ctx.h, "fmmt_op_save")
 
     def ranks(self) -> np.ndarray:
         cnt = C.c_int64()

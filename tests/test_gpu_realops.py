@@ -125,6 +125,40 @@ def test_export_import_roundtrip(fm, ctx, fmt, tol):
     op2.close()
 
 
+@pytest.mark.parametrize("fmt", ["dense", "tucker3d", "tucker4d", "htucker4d", "tt3d", "tt4d"])
+def test_save_load_roundtrip(fm, ctx, fmt, tmp_path):
+    """fmmt_op_save / fmmt_op_load (skip re-compression): the loaded op carries the same ranks
+    and factors and its matvec is bit-identical; a truncated or corrupted file is refused (FMMT_E_STATE)."""
+    c = config(2)
+    T4, _, _ = operator(2)
+    nd = 48
+    op = ctx.compress(lib_T(T4[..., :nd]), c.n, nd, fmt, 1e-4)
+    path = str(tmp_path / f"{fmt}.fmmtop")
+    op.save(path)
+    op2 = ctx.load_op(path)
+    assert np.array_equal(op.ranks(), op2.ranks())
+    for a0, a1 in zip(op.export(), op2.export()):
+        assert np.array_equal(a0, a1)
+    i0, i1 = op.info(), op2.info()
+    assert i0["compressed_bytes"] == i1["compressed_bytes"] and i0["format"] == i1["format"]
+    sig = signatures(signature_seed(2, 7), nd, c.Nx, c.Ny, c.Nz)
+    a = gpu_translate(ctx, op, sig, (c.Nx, c.Ny, c.Nz))
+    b = gpu_translate(ctx, op2, sig, (c.Nx, c.Ny, c.Nz))
+    assert np.array_equal(a, b)
+    op2.close()
+    raw = open(path, "rb").read()
+    bad = str(tmp_path / "bad.fmmtop")
+    flipped = bytearray(raw)
+    flipped[len(raw) // 2] ^= 0x10
+    for blob in (raw[:len(raw) // 2], raw[:-8], bytes(flipped), b"not an op file" * 8):
+        open(bad, "wb").write(blob)
+        with pytest.raises(fm.FmmtError, match="E_STATE"):
+            ctx.load_op(bad)
+    with pytest.raises(fm.FmmtError, match="E_STATE"):
+        ctx.load_op(str(tmp_path / "missing.fmmtop"))
+    op.close()
+
+
 def test_export_errors(fm, ctx):
     c = config(1)
     T4, _, _ = operator(1)
@@ -174,6 +208,45 @@ def test_virtual_sharding_sum(fm, ctx, fmt, tol):
     MARGINS[f"shard3/{fmt}"] = e
     assert e <= 1e-5, e
     full.close()
+
+
+@pytest.mark.parametrize("fmt", ["tt4d", "tucker4d", "htucker4d", "tucker3d"])
+def test_single_rank_communicator_runs_collectives(fm, ctx, fmt):
+    """The sharded call sequence on one GPU: a world-size-1 NCCL communicator
+    makes fmmt_compress take the 4D root path (compress all of T_4D, ncclBroadcast the rank header and the
+    factors, keep the shard's rows of the direction factor) and fmmt_translate_sum run its ncclAllReduce,
+    directly, during graph capture and on replay.  With one rank both collectives are the identity, so every
+    result must be bit-identical to the communicator-free context's."""
+    c = config(2)
+    T4, w, _ = operator(2)
+    nd = T4.shape[3]
+    N = (c.Nx, c.Ny, c.Nz)
+    Tl = torch.from_numpy(lib_T(T4)).cuda()
+    b, cnt = fm.shard_range(nd, 1, 3)
+    sig = torch.from_numpy(signatures(signature_seed(2, 6), nd, *N)[b:b + cnt]).cuda()
+    wd = torch.from_numpy(w.astype(np.float32)[b:b + cnt]).cuda()
+    plain = ctx.compress(Tl, c.n, nd, fmt, 1e-4, b, cnt)
+    ref = torch.empty(N[::-1], dtype=torch.complex64, device="cuda")
+    plain.translate_sum(sig, None, wd, ref, cnt, N)
+    ctx.sync()
+    sctx = fm.Context(0, torch.cuda.current_stream().cuda_stream, rank=0, world=1, nccl_id=fm.nccl_unique_id())
+    try:
+        sh = sctx.compress(Tl, c.n, nd, fmt, 1e-4, b, cnt)
+        assert np.array_equal(sh.ranks(), plain.ranks())
+        for a0, a1 in zip(sh.export(), plain.export()):
+            assert np.array_equal(a0, a1)
+        for it in range(4):   # direct run, capture, two replays
+            got = torch.full_like(ref, float("nan"))
+            sh.translate_sum(sig, None, wd, got, cnt, N)
+            sctx.sync()
+            assert torch.equal(got, ref), it
+        host = np.zeros(N[::-1], dtype=np.complex64)
+        sh.translate_sum_host(sig.cpu().numpy(), wd.cpu().numpy(), host, cnt, N)
+        assert np.array_equal(host, ref.cpu().numpy())
+        sh.close()
+    finally:
+        sctx.close()
+    plain.close()
 
 
 # ------------------------------------------------------------------ config 3 (elongated grid), all 338 directions
