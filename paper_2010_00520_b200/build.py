@@ -90,5 +90,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+def build_variant(tag: str, defs: list, verbose: bool = False) -> str:
+    """An experimental A/B build libfmmt_<tag>.so with extra -D flags (loaded with FMMT_LIB=<tag>)."""
+    out = os.path.join(HERE, f"libfmmt_{tag}.so")
+    job = _build_one(out, ["-DFMMT_TC_F16=1", *defs], verbose, True)
+    _finish(job, verbose)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force=True))

@@ -20,7 +20,10 @@
 
 namespace fmmt {
 
-constexpr int XYB_THREADS = 512;
+#ifndef FMMT_XYB_THREADS
+#define FMMT_XYB_THREADS 512
+#endif
+constexpr int XYB_THREADS = FMMT_XYB_THREADS;
 
 template <int NX, int NY, int PP>
 struct XYBig {

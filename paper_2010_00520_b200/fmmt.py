@@ -17,8 +17,10 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# FMMT_LIB=tf32 selects the TF32-split build of the same sources (A/B measurement only)
-LIB_PATH = os.path.join(_HERE, "libfmmt_tf32.so" if os.environ.get("FMMT_LIB") == "tf32" else "libfmmt.so")
+# FMMT_LIB=tf32 selects the TF32-split build of the same sources (A/B measurement only); any other tag an
+# experimental build libfmmt_<tag>.so made with build.build_variant(tag, defs)
+_TAG = os.environ.get("FMMT_LIB")
+LIB_PATH = os.path.join(_HERE, f"libfmmt_{_TAG}.so" if _TAG else "libfmmt.so")
 # operand split of the loaded build's restore contractions (3 tensor MMAs per useful MAC either way)
 SPLIT = "tf32" if os.environ.get("FMMT_LIB") == "tf32" else "fp16"
 
