@@ -132,6 +132,8 @@ static cudaError_t set_smem_once(const void* fn, int bytes) {
   auto it = done.find(fn);
   if (it != done.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  // the largest shared-memory carveout, so that kernels sized for two CTAs per SM get both resident
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess) done[fn] = bytes;
   return e;
 }
@@ -139,6 +141,7 @@ static cudaError_t set_smem_once(const void* fn, int bytes) {
 namespace {
 
 bool xy_big_enabled = true;   // FMMT_XY_BIG=0: the chunked four-step kernels for every plane size (A/B)
+bool xy_half_enabled = false; // FMMT_XY_HALF=0: the full-plane forward kernel for the one-plane-per-CTA sizes (A/B)
 
 struct XYKernels {
   void (*fwd)(const float2*, float2*, int, int) = nullptr;
@@ -147,6 +150,7 @@ struct XYKernels {
   int lines = 0;          // max concurrent line-items per plane (for planes-per-CTA)
   int big_pp = 0;         // > 0: whole-plane kernels (kernels_fft_big.cuh), big_pp planes per 512-thread CTA
   int big_smem = 0;       // their dynamic shared memory (bytes)
+  int big_smem_fwd = 0;   // the forward kernel's when it differs (half-buffer kernel, one plane per CTA)
 };
 
 // planes per CTA of the whole-plane kernels: the most of {4, 2, 1} whose buffers fit ~210 KB (0: none fits)
@@ -166,6 +170,15 @@ XYKernels make_xy_big(XYKernels k) {
     k.inv = fmmt::k_inv_xy_big<NX, NY, PP>;
     k.big_pp = PP;
     k.big_smem = fmmt::XYBig<NX, NY, PP>::SMEM;
+    k.big_smem_fwd = k.big_smem;
+    if constexpr (PP == 1) {
+      if (xy_half_enabled) {
+        k.fwd = fmmt::k_fwd_xy_half<NX, NY>;
+        k.big_smem_fwd = fmmt::XYHalf<NX, NY>::SMEM;
+        k.inv = fmmt::k_inv_xy_half<NX, NY>;
+        k.big_smem = fmmt::XYInvHalf<NX, NY>::SMEM;
+      }
+    }
   }
   return k;
 }
@@ -1149,7 +1162,7 @@ static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* ou
   if (k.big_pp) {
     threads = fmmt::XYB_THREADS;
     ppc = k.big_pp;
-    smem = (size_t)k.big_smem;
+    smem = (size_t)(fwd ? k.big_smem_fwd : k.big_smem);
   }
   const unsigned grid = (unsigned)((nplanes + ppc - 1) / ppc);
   ProfScope ps(ctx, fwd ? "fft_fwd_xy" : "fft_inv_xy");
@@ -1579,6 +1592,7 @@ fmmt_status fmmt_init_sharded(int device, void* cuda_stream, int rank, int world
   if (const char* e = getenv("FMMT_W_MB")) ctx->w_mb = std::max(1, atoi(e));
   if (const char* e = getenv("FMMT_ZCLUSTER")) ctx->z_cluster = atoi(e) != 0;
   if (const char* e = getenv("FMMT_XY_BIG")) xy_big_enabled = atoi(e) != 0;
+  if (const char* e = getenv("FMMT_XY_HALF")) xy_half_enabled = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZFUSE")) ctx->z_fuse = atoi(e) != 0;
   if (const char* e = getenv("FMMT_ZFC")) ctx->z_fc = atoi(e);
   if (const char* e = getenv("FMMT_H2D_OVERLAP")) ctx->h2d_overlap = atoi(e) != 0;

@@ -131,6 +131,125 @@ k_fwd_xy_big(const float2* __restrict__ sig_in, float2* __restrict__ W, int npla
   }
 }
 
+// Half-buffer forward kernel for the one-plane-per-CTA sizes (128 x 128, 256 x 64, 64 x 256): the x pass only
+// ever fills the Ny nonzero rows, and the y pass keeps in shared memory only the k1 < AY / 2 half of its
+// intermediate (written back to exactly the rows it was read from); the other half waits in registers until the
+// first half's pass 2 has gone out to W.  66 KB instead of 132 KB of shared memory -> two CTAs per SM, so one
+// CTA's prologue, global loads and barrier tails run under the other's DFTs.
+template <int NX, int NY>
+struct XYHalf {
+  static constexpr int PX = NX + 1;
+  static constexpr int SMEM = ((NY / 2) * PX + NX + NY) * 8;
+};
+
+template <int NX, int NY>
+__global__ void __launch_bounds__(XYB_THREADS, 2)
+k_fwd_xy_half(const float2* __restrict__ sig_in, float2* __restrict__ W, int nplanes_total, int) {
+  using G = XYBig<NX, NY, 1>;
+  constexpr int Nx = G::Nx, Ny = G::Ny, PX = G::PX, AX = G::AX, BX = G::BX, AY = G::AY, BY = G::BY;
+  extern __shared__ float2 smem[];
+  float2* buf = smem;
+  float2* twx = smem + Ny * PX;
+  float2* twy = twx + NX;
+  const int g = blockIdx.x;
+  if (g >= nplanes_total) return;
+  load_fourstep_tw<NX>(twx);
+  load_fourstep_tw<NY>(twy);
+  __syncthreads();
+  // x pass 1 (sig_in -> smem), item (y, n2), n2 fastest
+  for (int it = threadIdx.x; it < Ny * BX; it += XYB_THREADS) {
+    const int n2 = it % BX, y = it / BX;
+    const float2* row = sig_in + ((int64_t)g * Ny + y) * Nx;
+    float2 v[AX];
+#pragma unroll
+    for (int n1 = 0; n1 < AX / 2; ++n1) v[n1] = row[BX * n1 + n2];
+    fft_reg<AX, false, true>(v);
+    float2* srow = buf + y * PX;
+#pragma unroll
+    for (int k1 = 0; k1 < AX; ++k1) srow[BX * k1 + n2] = k1 ? cmul(v[k1], twx[k1 * BX + n2]) : v[k1];
+  }
+  __syncthreads();
+  // x pass 2, item (y, k1), y fastest
+  {
+    constexpr int IPT = (Ny * AX + XYB_THREADS - 1) / XYB_THREADS;
+    float2 v[IPT][BX];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < Ny * AX) {
+        const int y = it % Ny, k1 = it / Ny;
+        const float2* srow = buf + y * PX;
+#pragma unroll
+        for (int n2 = 0; n2 < BX; ++n2) v[u][n2] = srow[BX * k1 + n2];
+        fft_reg<BX, false, false>(v[u]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < Ny * AX) {
+        const int y = it % Ny, k1 = it / Ny;
+        float2* srow = buf + y * PX;
+#pragma unroll
+        for (int k2 = 0; k2 < BX; ++k2) srow[k1 + AX * k2] = v[u][k2];
+      }
+    }
+  }
+  __syncthreads();
+  // y pass 1, item (x, n2), x fastest: rows BY n1 + n2 (n1 < AY / 2) -> the same rows for k1 < AY / 2, in place;
+  // k1 >= AY / 2 held in registers
+  constexpr int IPT1 = (NX * BY + XYB_THREADS - 1) / XYB_THREADS;
+  float2 hold[IPT1][AY / 2];
+#pragma unroll
+  for (int u = 0; u < IPT1; ++u) {
+    const int it = threadIdx.x + u * XYB_THREADS;
+    if (it < NX * BY) {
+      const int x = it % NX, n2 = it / NX;
+      float2* col = buf + x;
+      float2 v[AY];
+#pragma unroll
+      for (int n1 = 0; n1 < AY / 2; ++n1) v[n1] = col[(BY * n1 + n2) * PX];
+      fft_reg<AY, false, true>(v);
+#pragma unroll
+      for (int k1 = 0; k1 < AY / 2; ++k1) col[(BY * k1 + n2) * PX] = k1 ? cmul(v[k1], twy[k1 * BY + n2]) : v[k1];
+#pragma unroll
+      for (int k1 = AY / 2; k1 < AY; ++k1) hold[u][k1 - AY / 2] = cmul(v[k1], twy[k1 * BY + n2]);
+    }
+  }
+  __syncthreads();
+  // y pass 2 (smem -> W), item (x, kk), x fastest, k1 = kk + h AY / 2: W[ky = k1 + AY k2][x]
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1) {
+      __syncthreads();   // every read of the first half is done
+#pragma unroll
+      for (int u = 0; u < IPT1; ++u) {
+        const int it = threadIdx.x + u * XYB_THREADS;
+        if (it < NX * BY) {
+          const int x = it % NX, n2 = it / NX;
+          float2* col = buf + x;
+#pragma unroll
+          for (int kk = 0; kk < AY / 2; ++kk) col[(BY * kk + n2) * PX] = hold[u][kk];
+        }
+      }
+      __syncthreads();
+    }
+    for (int it = threadIdx.x; it < NX * (AY / 2); it += XYB_THREADS) {
+      const int x = it % NX, kk = it / NX, k1 = kk + h * (AY / 2);
+      const float2* col = buf + x;
+      float2 v[BY];
+#pragma unroll
+      for (int n2 = 0; n2 < BY; ++n2) v[n2] = col[(BY * kk + n2) * PX];
+      fft_reg<BY, false, false>(v);
+      float2* out = W + (int64_t)g * (NX * NY) + x;
+#pragma unroll
+      for (int k2 = 0; k2 < BY; ++k2) out[(int64_t)(k1 + AY * k2) * NX] = v[k2];
+    }
+  }
+}
+
+
 template <int NX, int NY, int PP>
 __global__ void __launch_bounds__(XYB_THREADS, 1)
 k_inv_xy_big(const float2* __restrict__ W, float2* __restrict__ sig_out, int nplanes_total, int, float scale) {
@@ -239,6 +358,167 @@ k_inv_xy_big(const float2* __restrict__ W, float2* __restrict__ sig_out, int npl
     for (int e = threadIdx.x; e < np * Nx * Ny; e += XYB_THREADS) {
       const int x = e % Nx, r = e / Nx, y = r % Ny, j = r / Ny;
       dst[e] = buf[j * G::PLANE + y * PX + x];
+    }
+  }
+}
+
+// Three-quarter-buffer inverse kernel for the same sizes: the y pass keeps the k1 < AY / 2 half of its
+// intermediate in NY / 2 rows (the other half in registers), writes that half's truncated outputs to an extra
+// NY / 4 rows, then runs the second half through the same NY / 2 rows.  The Ny surviving rows end up permuted
+// (row_of): the x pass works row by row, so only its row addressing and the final store see the permutation.
+// The extra region starts 8 rows late so that 16 consecutive y still fall into 16 different bank pairs.
+template <int NX, int NY>
+struct XYInvHalf {
+  static constexpr int PX = NX + 1;
+  static constexpr int AY = Split<NY>::A, BY = Split<NY>::B;
+  static constexpr int EXTRA = NY / 2 + 8;
+  static constexpr int ROWS = EXTRA + NY / 4;
+  static constexpr int SMEM = (ROWS * PX + NX + NY) * 8;
+  __device__ static __forceinline__ int row_of(int y) {
+    const int k1 = y % AY, k2 = y / AY;
+    return k1 < AY / 2 ? EXTRA + k1 + (AY / 2) * k2 : (k1 - AY / 2) + (AY / 2) * k2;
+  }
+};
+
+template <int NX, int NY>
+__global__ void __launch_bounds__(XYB_THREADS, 2)
+k_inv_xy_half(const float2* __restrict__ W, float2* __restrict__ sig_out, int nplanes_total, int, float scale) {
+  using G = XYBig<NX, NY, 1>;
+  using H = XYInvHalf<NX, NY>;
+  constexpr int Nx = G::Nx, Ny = G::Ny, PX = G::PX, AX = G::AX, BX = G::BX, AY = G::AY, BY = G::BY;
+  extern __shared__ float2 smem[];
+  float2* buf = smem;
+  float2* twx = smem + H::ROWS * PX;
+  float2* twy = twx + NX;
+  const int g = blockIdx.x;
+  if (g >= nplanes_total) return;
+  load_fourstep_tw<NX>(twx);
+  load_fourstep_tw<NY>(twy);
+  __syncthreads();
+  // y pass 1 (W -> smem rows BY k1 + n2 for k1 < AY / 2, registers for the rest), item (x, n2), x fastest
+  constexpr int IPT1 = (NX * BY + XYB_THREADS - 1) / XYB_THREADS;
+  float2 hold[IPT1][AY / 2];
+#pragma unroll
+  for (int u = 0; u < IPT1; ++u) {
+    const int it = threadIdx.x + u * XYB_THREADS;
+    if (it < NX * BY) {
+      const int x = it % NX, n2 = it / NX;
+      const float2* in = W + (int64_t)g * (NX * NY) + x;
+      float2 v[AY];
+#pragma unroll
+      for (int n1 = 0; n1 < AY; ++n1) v[n1] = in[(int64_t)(BY * n1 + n2) * NX];
+      fft_reg<AY, true, false>(v);
+      float2* col = buf + x;
+#pragma unroll
+      for (int k1 = 0; k1 < AY / 2; ++k1) col[(BY * k1 + n2) * PX] = k1 ? cmul(v[k1], conjf2(twy[k1 * BY + n2])) : v[k1];
+#pragma unroll
+      for (int k1 = AY / 2; k1 < AY; ++k1) hold[u][k1 - AY / 2] = cmul(v[k1], conjf2(twy[k1 * BY + n2]));
+    }
+  }
+  __syncthreads();
+  // y pass 2, first half: item (x, kk), outputs y = kk + AY k2 < Ny (k2 < BY / 2) go straight to the extra rows
+  for (int it = threadIdx.x; it < NX * (AY / 2); it += XYB_THREADS) {
+    const int x = it % NX, kk = it / NX;
+    float2* col = buf + x;
+    float2 v[BY];
+#pragma unroll
+    for (int n2 = 0; n2 < BY; ++n2) v[n2] = col[(BY * kk + n2) * PX];
+    fft_reg<BY, true, false>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < BY / 2; ++k2) col[(H::EXTRA + kk + (AY / 2) * k2) * PX] = v[k2];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < IPT1; ++u) {
+    const int it = threadIdx.x + u * XYB_THREADS;
+    if (it < NX * BY) {
+      const int x = it % NX, n2 = it / NX;
+      float2* col = buf + x;
+#pragma unroll
+      for (int kk = 0; kk < AY / 2; ++kk) col[(BY * kk + n2) * PX] = hold[u][kk];
+    }
+  }
+  __syncthreads();
+  // second half (k1 = kk + AY / 2): outputs held over a barrier, then written to rows kk + (AY / 2) k2
+  {
+    constexpr int IPT2 = (NX * (AY / 2) + XYB_THREADS - 1) / XYB_THREADS;
+    float2 o[IPT2][BY / 2];
+#pragma unroll
+    for (int u = 0; u < IPT2; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < NX * (AY / 2)) {
+        const int x = it % NX, kk = it / NX;
+        const float2* col = buf + x;
+        float2 v[BY];
+#pragma unroll
+        for (int n2 = 0; n2 < BY; ++n2) v[n2] = col[(BY * kk + n2) * PX];
+        fft_reg<BY, true, false>(v);
+#pragma unroll
+        for (int k2 = 0; k2 < BY / 2; ++k2) o[u][k2] = v[k2];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT2; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < NX * (AY / 2)) {
+        const int x = it % NX, kk = it / NX;
+        float2* col = buf + x;
+#pragma unroll
+        for (int k2 = 0; k2 < BY / 2; ++k2) col[(kk + (AY / 2) * k2) * PX] = o[u][k2];
+      }
+    }
+  }
+  __syncthreads();
+  // x pass 1 on the Ny surviving rows, item (y, n2), y fastest: full input
+  for (int it = threadIdx.x; it < Ny * BX; it += XYB_THREADS) {
+    const int y = it % Ny, n2 = it / Ny;
+    float2* srow = buf + H::row_of(y) * PX;
+    float2 v[AX];
+#pragma unroll
+    for (int n1 = 0; n1 < AX; ++n1) v[n1] = srow[BX * n1 + n2];
+    fft_reg<AX, true, false>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < AX; ++k1) srow[BX * k1 + n2] = k1 ? cmul(v[k1], conjf2(twx[k1 * BX + n2])) : v[k1];
+  }
+  __syncthreads();
+  // x pass 2, item (y, k1), y fastest: outputs x = k1 + AX k2 < Nx (k2 < BX / 2), scaled
+  {
+    constexpr int IPT = (Ny * AX + XYB_THREADS - 1) / XYB_THREADS;
+    float2 o[IPT][BX / 2];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < Ny * AX) {
+        const int y = it % Ny, k1 = it / Ny;
+        const float2* srow = buf + H::row_of(y) * PX;
+        float2 v[BX];
+#pragma unroll
+        for (int n2 = 0; n2 < BX; ++n2) v[n2] = srow[BX * k1 + n2];
+        fft_reg<BX, true, false>(v);
+#pragma unroll
+        for (int k2 = 0; k2 < BX / 2; ++k2) o[u][k2] = cscale(v[k2], scale);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+      const int it = threadIdx.x + u * XYB_THREADS;
+      if (it < Ny * AX) {
+        const int y = it % Ny, k1 = it / Ny;
+        float2* srow = buf + H::row_of(y) * PX;
+#pragma unroll
+        for (int k2 = 0; k2 < BX / 2; ++k2) srow[k1 + AX * k2] = o[u][k2];
+      }
+    }
+  }
+  __syncthreads();
+  // store rows y < Ny, x < Nx (coalesced along x)
+  {
+    float2* dst = sig_out + (int64_t)g * (Nx * Ny);
+    for (int e = threadIdx.x; e < Nx * Ny; e += XYB_THREADS) {
+      const int x = e % Nx, y = e / Nx;
+      dst[e] = buf[H::row_of(y) * PX + x];
     }
   }
 }
