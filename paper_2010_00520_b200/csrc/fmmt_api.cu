@@ -125,15 +125,16 @@ static void prof_flush(fmmt_ctx* ctx) {
 // ============================================================== kernel dispatch
 // Raise a kernel's dynamic shared-memory limit once per process (not per launch:
 // the call is host-side work on the launch path and must stay out of graph capture).
-static cudaError_t set_smem_once(const void* fn, int bytes) {
+static cudaError_t set_smem_once(const void* fn, int bytes, bool max_carveout = false) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> done;
   std::lock_guard<std::mutex> lk(mu);
   auto it = done.find(fn);
   if (it != done.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  // the largest shared-memory carveout, so that kernels sized for two CTAs per SM get both resident
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // the largest shared-memory carveout for kernels sized so that two CTAs share an SM
+  if (e == cudaSuccess && max_carveout)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess) done[fn] = bytes;
   return e;
 }
@@ -141,7 +142,7 @@ static cudaError_t set_smem_once(const void* fn, int bytes) {
 namespace {
 
 bool xy_big_enabled = true;   // FMMT_XY_BIG=0: the chunked four-step kernels for every plane size (A/B)
-bool xy_half_enabled = false; // FMMT_XY_HALF=0: the full-plane forward kernel for the one-plane-per-CTA sizes (A/B)
+bool xy_half_enabled = true;   // FMMT_XY_HALF=0: the full-plane kernels for the one-plane-per-CTA sizes (A/B)
 
 struct XYKernels {
   void (*fwd)(const float2*, float2*, int, int) = nullptr;
@@ -1167,10 +1168,10 @@ static fmmt_status launch_xy(fmmt_op* op, bool fwd, const float2* in, float2* ou
   const unsigned grid = (unsigned)((nplanes + ppc - 1) / ppc);
   ProfScope ps(ctx, fwd ? "fft_fwd_xy" : "fft_inv_xy");
   if (fwd) {
-    FMMT_CUDA(ctx, set_smem_once((const void*)k.fwd, (int)smem));
+    FMMT_CUDA(ctx, set_smem_once((const void*)k.fwd, (int)smem, k.big_pp == 1));
     k.fwd<<<grid, threads, smem, ctx->stream>>>(in, out, nplanes, ppc);
   } else {
-    FMMT_CUDA(ctx, set_smem_once((const void*)k.inv, (int)smem));
+    FMMT_CUDA(ctx, set_smem_once((const void*)k.inv, (int)smem, k.big_pp == 1));
     k.inv<<<grid, threads, smem, ctx->stream>>>(in, out, nplanes, ppc, scale);
   }
   FMMT_CUDA(ctx, cudaGetLastError());
