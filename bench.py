@@ -639,7 +639,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(len(res["ops"]) * (res["dn"] * K * 8 + res["dn"] * 4)),
                 "d2h_bytes_per_step": int(len(res["ops"]) * K * 8),
-                "note": "fmmt_translate_sum_host per op: pinned host signatures + weights in, direction sum out"},
+                "note": "fmmt_translate_sum_host per op: pinned host signatures + weights in (chunked upload on a copy stream, overlapped with the matvec), direction sum out"},
         "per_box": {"value": round(head["value"] / 8, 3), "unit": "Gdir*box/s",
                     "note": "the same rate per box of the Nx*Ny*Nz grid (8 padded points per box)"},
         "dense": head.get("dense"),

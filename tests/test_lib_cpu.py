@@ -85,3 +85,14 @@ def test_errors_without_gpu(lib):
         lib.multipole_count(-1.0, 0.5, 3)
     with pytest.raises(lib.FmmtError):
         lib.shard_range(10, 3, 2)
+
+
+def test_null_handles_rejected_without_gpu(lib, tmp_path):
+    # serialisation and the host-buffer matvec refuse null handles before touching a device or a file
+    path = str(tmp_path / "x.fmmtop").encode()
+    out = lib.vp()
+    assert lib.fmmt_op_save(None, path) == 1            # FMMT_E_ARG
+    assert lib.fmmt_op_load(None, path, lib.C.byref(out)) == 1
+    assert not out.value
+    assert not (tmp_path / "x.fmmtop").exists()
+    assert lib.fmmt_translate_sum_host(None, None, None, None, 1, 1, 1, 1) == 1
